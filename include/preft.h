@@ -1,0 +1,223 @@
+/*
+ * preft.h — C ABI of libpreft, the B200 (sm_100a) PreFT hot path.
+ *
+ * The reference (arxiv 2605.14217, package `prefillsim`) is pure Python; its
+ * "FFI" for this path is the Python operator API.  Each entry point below
+ * replaces one piece of that API (file:line relative to /root/reference):
+ *
+ *   preft_meta_build      <- compute_position_mask   pkg/src/prefillsim/model.py:305-319
+ *                            (+ the per-entry row selection inside
+ *                             forward_chunk, model.py:474-475,509,538; the
+ *                             grouping of selected tokens by adapter has no
+ *                             reference counterpart)
+ *   preft_lora_apply      <- _project's low-rank delta  model.py:442-452
+ *                            via delta_for_rows        adapters.py:278-288
+ *                            (in place on the base output y; one call covers
+ *                             every entry of the batch and 1-3 sites that
+ *                             share the same input x: q/k/v, gate/up)
+ *   preft_reft_apply      <- the residual-stream hook   model.py:543-546
+ *                            via delta_for_rows        adapters.py:289-295
+ *                            (DiReFT and LoReFT; LoReFT arrives with
+ *                             A := W - R folded at registration)
+ *   preft_convert_2d      <- AdapterParams construction adapters.py:129-185
+ *                            (f64 bundle -> bf16/f32 pool slab slot; the
+ *                             upload half of weight sync, engine.py:676-697)
+ *
+ * Conventions
+ *   - every pointer argument is a DEVICE pointer unless stated otherwise;
+ *   - every call is stream-ordered on `stream` (a cudaStream_t passed as
+ *     void*), never synchronises the host, and is CUDA-graph capturable:
+ *     sizes that change per step (E, T) are read from device memory;
+ *   - return value 0 = success, otherwise a PREFT_ERR_* code.  Codes 1-8 map
+ *     one-to-one onto prefillsim.errors (errors.py:8-37); the Python shim
+ *     raises the matching exception class.
+ */
+#ifndef PREFT_H
+#define PREFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PREFT_ABI_VERSION 1
+
+/* status codes (errors.py:8-37) */
+#define PREFT_OK 0
+#define PREFT_ERR_SHAPE 1      /* ShapeError  */
+#define PREFT_ERR_RANK 2       /* RankError   */
+#define PREFT_ERR_DOMAIN 3     /* DomainError */
+#define PREFT_ERR_CONFIG 4     /* ConfigError */
+#define PREFT_ERR_BATCH 5      /* BatchError  */
+#define PREFT_ERR_STATE 6      /* StateError  */
+#define PREFT_ERR_SYNC 7       /* SyncError   */
+#define PREFT_ERR_INFEASIBLE 8 /* InfeasibleBatchError */
+#define PREFT_ERR_CUDA 16      /* a CUDA runtime/launch error (RuntimeError) */
+
+/* element types of activations and pool slabs */
+#define PREFT_DTYPE_F32 0  /* fp32 I/O, fp32 accumulate: the "fp32 mode" (<= 1e-5 rel)   */
+#define PREFT_DTYPE_BF16 1 /* bf16 I/O, fp32 accumulate: the serving mode (<= 2e-2 rel)  */
+#define PREFT_DTYPE_F64 2  /* f64 I/O, f64 accumulate: the reference's own precision     */
+
+/* per-entry flag bits (SeqEntry.phase / .schedule, model.py:223-242) */
+#define PREFT_ENTRY_DECODE 1        /* Phase.DECODE (else PREFILL) */
+#define PREFT_ENTRY_ALL_POSITIONS 2 /* PositionSchedule.ALL_POSITIONS */
+
+/* device-side error bits written to counters[PREFT_CTR_ERR] by preft_meta_build */
+#define PREFT_META_ERR_E_RANGE 1   /* E < 1 or E > E_cap            */
+#define PREFT_META_ERR_T_RANGE 2   /* T < 1 or T > T_cap            */
+#define PREFT_META_ERR_QSL 4       /* query_start_loc not a strictly increasing prefix sum from 0 to T */
+#define PREFT_META_ERR_TILES 8     /* work list would exceed tile_cap */
+
+/* counters[] slots */
+#define PREFT_CTR_SEL_TOKENS 0  /* selected (adapter-carrying) tokens      */
+#define PREFT_CTR_SEGMENTS 1    /* segments = runs of one adapter slot      */
+#define PREFT_CTR_TILES 2       /* work tiles of <= tile_tokens tokens      */
+#define PREFT_CTR_ERR 3         /* PREFT_META_ERR_* bits                    */
+#define PREFT_CTR_SEL_ENTRIES 4 /* entries whose tokens are selected        */
+#define PREFT_CTR_T 5           /* T as read from the entry buffer          */
+#define PREFT_CTR_E 6           /* E as read from the entry buffer          */
+#define PREFT_CTR_SPLIT 7       /* selected tokens whose slot < slot_split  */
+#define PREFT_NUM_COUNTERS 8
+
+/*
+ * Batch-metadata workspace.  All arrays are device memory at fixed addresses
+ * (allocated once by the host, reused every step, so a captured CUDA graph
+ * stays valid).  The host writes `entries` (one H2D copy per step):
+ *
+ *   entries[0]                 = E  (number of SeqEntry)
+ *   entries[1]                 = T  (total query tokens)
+ *   entries[2 .. 2+E]          = query_start_loc[0..E]      (model.py:248)
+ *   entries[3+E .. 3+2E)       = adapter slot per entry, -1 = no adapter
+ *   entries[3+2E .. 3+3E)      = PREFT_ENTRY_* flags per entry
+ *
+ * preft_meta_build fills:
+ *   mask[T]            1 where the reference's PositionMask is True (bit-exact)
+ *   tokens[2*n_sel]    (token index, slot) pairs of the selected tokens, stably
+ *                      sorted by slot (ties keep batch order)
+ *   segments[3*nseg]   (slot, first sorted position, length)
+ *   tiles[4*ntiles]    (slot, first sorted position, n tokens, segment id)
+ *   entry_offset[E]    sorted position of the entry's first token, -1 if unselected
+ *   counters[8]        PREFT_CTR_*
+ *
+ * Slot classes: one pool serves LoRA and ReFT adapters side by side (a batch
+ * may mix them, BASELINE config 1).  LoRA adapters own slots [0, slot_split),
+ * ReFT adapters slots [slot_split, ...).  Because tokens are sorted by slot,
+ * the LoRA tokens are sorted positions [0, counters[SPLIT]) and the ReFT
+ * tokens [counters[SPLIT], counters[SEL_TOKENS]): preft_lora_apply walks the
+ * first range, preft_reft_apply the second (indexing its slabs with
+ * slot - slot_split).
+ */
+typedef struct preft_meta {
+    int32_t* entries;
+    uint8_t* mask;
+    int32_t* tokens;
+    int32_t* segments;
+    int32_t* tiles;
+    int32_t* entry_offset;
+    int32_t* counters;
+    int32_t E_cap;       /* <= PREFT_MAX_ENTRIES */
+    int32_t T_cap;
+    int32_t tile_cap;    /* >= E_cap + T_cap / tile_tokens + 1 */
+    int32_t tile_tokens; /* tokens per work tile (>= 1) */
+    int32_t slot_split;  /* first ReFT slot; slots below it are LoRA slots */
+    int32_t reserved;
+} preft_meta_t;
+
+#define PREFT_MAX_ENTRIES 4096
+
+/* number of int32 words `entries` must hold for E_cap entries */
+size_t preft_meta_entries_words(int32_t E_cap);
+
+/* K1: device metadata builder (replaces compute_position_mask, model.py:305). */
+int preft_meta_build(const preft_meta_t* meta, void* stream);
+
+/*
+ * One LoRA site of a fused group (all sites of a group read the same x).
+ * Pool layout for this (layer, site): A  [S][r_max][m], Bt [S][r_max][n]
+ * (the reference's B is (n, r), adapters.py:159; it is stored transposed so
+ * the expand streams contiguous rows), scale [S] = scaling_prefactor
+ * (adapters.py:109-117) in the accumulator type (f32 for F32/BF16, f64 for
+ * F64).  Rows k >= rank of a slot are zero.
+ */
+typedef struct preft_lora_site {
+    const void* A;
+    const void* Bt;
+    const void* scale;
+    const void* bias; /* NULL, or [S][r_max] added to the rank-r intermediate before
+                         the scale (lets this kernel compute the ReFT delta
+                         s*((h A^T + b) B) out of place, adapters.py:292-295) */
+    void* y;        /* base output [T][ldy], updated in place on selected rows */
+    int64_t ldy;
+    int32_t n;
+    int32_t reserved;
+} preft_lora_site_t;
+
+/*
+ * K2: y_s[t,:] += s_a * (x[t,:] . A_s,a^T) . Bt_s,a   for every selected token t
+ * (adapter a = its slot) and every site s of the group (adapters.py:288).
+ * Unselected rows of y are never read or written.
+ *   x: [T][ldx] (dtype), m = input width; nsites in 1..3; r_max in
+ *   {1,2,4,8,16,32,64} with nsites * r_max <= 64.
+ */
+int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32_t m,
+                     const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
+                     int32_t dtype, void* stream);
+
+/*
+ * K3: h[t,:] += s_a * ((h[t,:] . A_a^T + b_a) . B_a)   for every selected token
+ * (adapters.py:292-295).  DiReFT: A, B as stored by the reference.  LoReFT:
+ * A = W - R, B = R.  Pool layout for this layer: A [S][r_max][d],
+ * B [S][r_max][d], bias [S][r_max], scale [S] (bias/scale in the accumulator
+ * type: f32 for F32/BF16, f64 for F64).  r_max in {1,2,4,8,16,32,64}.
+ */
+int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t ldh, int32_t d,
+                     const void* A, const void* B, const void* bias, const void* scale,
+                     int32_t r_max, int32_t dtype, void* stream);
+
+/*
+ * K4: dst[i*dst_ld + j] = convert(src[i*src_stride_row + j*src_stride_col])
+ * for i < rows_valid, j < cols; rows in [rows_valid, rows) are zero-filled.
+ * src is a DEVICE float64 buffer; round-to-nearest-even into dst_dtype.
+ */
+int preft_convert_2d(void* dst, int32_t dst_dtype, int64_t dst_ld, const double* src,
+                     int64_t src_stride_row, int64_t src_stride_col, int64_t rows_valid,
+                     int64_t rows, int64_t cols, void* stream);
+
+/*
+ * Step plan: the native executor that replaces forward_chunk's Python
+ * `layer x entry` loop (model.py:504-546).  A plan holds a copy of the meta
+ * descriptor and an ordered list of LoRA-group / ReFT launches with fixed
+ * pointers; preft_plan_run issues K1 (optional) and every launch on `stream`
+ * with one call, and is CUDA-graph capturable while timing is off.  Launches
+ * whose `tag` equals the timing tag are bracketed by CUDA events (bench.py's
+ * per-kernel roofline figure).
+ */
+typedef struct preft_plan preft_plan_t;
+preft_plan_t* preft_plan_create(const preft_meta_t* meta);
+void preft_plan_destroy(preft_plan_t* plan);
+int preft_plan_set_slot_split(preft_plan_t* plan, int32_t slot_split);
+int preft_plan_add_lora(preft_plan_t* plan, const void* x, int64_t ldx, int32_t m,
+                        const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
+                        int32_t dtype, int32_t tag);
+int preft_plan_add_reft(preft_plan_t* plan, void* h, int64_t ldh, int32_t d, const void* A,
+                        const void* B, const void* bias, const void* scale, int32_t r_max,
+                        int32_t dtype, int32_t tag);
+int preft_plan_num_ops(const preft_plan_t* plan);
+int preft_plan_set_timing(preft_plan_t* plan, int32_t tag, int32_t reserve_pairs);
+int preft_plan_run(preft_plan_t* plan, int32_t run_meta, void* stream);
+int preft_plan_collect_timing(preft_plan_t* plan, double* total_ms, int32_t* count);
+
+/* library / device introspection */
+int preft_abi_version(void);
+const char* preft_status_string(int status);
+const char* preft_last_cuda_error(void);
+int preft_num_sms(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PREFT_H */

@@ -1,0 +1,173 @@
+// extern "C" surface of libpreft (declared in include/preft.h) and K4, the
+// f64 -> pool-slab conversion used by adapter registration / weight sync.
+#include <cstdio>
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+
+namespace preft {
+
+int meta_build(const preft_meta_t* m, cudaStream_t stream, int num_sms);
+int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
+               int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
+int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
+               const void* bias, const void* scale, int r, int dtype, cudaStream_t stream, int num_sms);
+
+static thread_local char g_last_cuda_error[256] = "";
+
+static int record_cuda(cudaError_t e) {
+    snprintf(g_last_cuda_error, sizeof(g_last_cuda_error), "%s: %s", cudaGetErrorName(e), cudaGetErrorString(e));
+    return PREFT_ERR_CUDA;
+}
+
+// kernel launch helpers return 0, a PREFT_ERR_* code (> 0) or -cudaError_t
+static int finish(int rc) {
+    if (rc < 0) return record_cuda(static_cast<cudaError_t>(-rc));
+    return rc;
+}
+
+static int current_num_sms() {
+    static std::mutex mu;
+    static std::unordered_map<int, int> cache;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    int sms = 148;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
+    cache[dev] = sms;
+    return sms;
+}
+
+// persistent grid: SM count x resident CTAs per SM for this kernel
+int grid_for(const void* fn, int threads, int num_sms) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cache;
+    int per_sm = 0;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        auto it = cache.find(fn);
+        if (it != cache.end()) per_sm = it->second;
+    }
+    if (per_sm == 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, 0) != cudaSuccess || per_sm < 1)
+            per_sm = 1;
+        std::lock_guard<std::mutex> lock(mu);
+        cache[fn] = per_sm;
+    }
+    return num_sms * per_sm;
+}
+
+int plan_num_sms() { return current_num_sms(); }
+int plan_record_cuda(cudaError_t e) { return record_cuda(e); }
+
+template <typename T>
+__device__ __forceinline__ T cvt_from_f64(double v);
+template <>
+__device__ __forceinline__ float cvt_from_f64<float>(double v) {
+    return __double2float_rn(v);
+}
+template <>
+__device__ __forceinline__ double cvt_from_f64<double>(double v) {
+    return v;
+}
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt_from_f64<__nv_bfloat16>(double v) {
+    // single rounding f64 -> bf16 (round to nearest even), no double rounding via f32
+    return __double2bfloat16(v);
+}
+
+template <typename T>
+__global__ void convert_2d_kernel(T* dst, long long dst_ld, const double* src, long long srow, long long scol,
+                                  long long rows_valid, long long rows, long long cols) {
+    const long long total = rows * cols;
+    for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+         idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+        const long long i = idx / cols, j = idx % cols;
+        const double v = i < rows_valid ? src[i * srow + j * scol] : 0.0;
+        dst[i * dst_ld + j] = cvt_from_f64<T>(v);
+    }
+}
+
+}  // namespace preft
+
+using namespace preft;
+
+extern "C" {
+
+int preft_abi_version(void) { return PREFT_ABI_VERSION; }
+
+const char* preft_status_string(int status) {
+    switch (status) {
+        case PREFT_OK: return "ok";
+        case PREFT_ERR_SHAPE: return "ShapeError";
+        case PREFT_ERR_RANK: return "RankError";
+        case PREFT_ERR_DOMAIN: return "DomainError";
+        case PREFT_ERR_CONFIG: return "ConfigError";
+        case PREFT_ERR_BATCH: return "BatchError";
+        case PREFT_ERR_STATE: return "StateError";
+        case PREFT_ERR_SYNC: return "SyncError";
+        case PREFT_ERR_INFEASIBLE: return "InfeasibleBatchError";
+        case PREFT_ERR_CUDA: return "CudaError";
+        default: return "unknown";
+    }
+}
+
+const char* preft_last_cuda_error(void) { return g_last_cuda_error; }
+
+int preft_num_sms(void) { return current_num_sms(); }
+
+size_t preft_meta_entries_words(int32_t E_cap) { return 2 + static_cast<size_t>(E_cap) * 3 + 1; }
+
+int preft_meta_build(const preft_meta_t* meta, void* stream) {
+    if (!meta || !meta->entries || !meta->mask || !meta->tokens || !meta->segments || !meta->tiles ||
+        !meta->entry_offset || !meta->counters)
+        return PREFT_ERR_SHAPE;
+    if (meta->E_cap < 1 || meta->E_cap > PREFT_MAX_ENTRIES || meta->T_cap < 1 || meta->tile_tokens < 1)
+        return PREFT_ERR_CONFIG;
+    if (static_cast<long long>(meta->tile_cap) <
+        static_cast<long long>(meta->E_cap) + meta->T_cap / meta->tile_tokens + 1)
+        return PREFT_ERR_CONFIG;
+    return finish(meta_build(meta, static_cast<cudaStream_t>(stream), current_num_sms()));
+}
+
+int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32_t m, const preft_lora_site_t* sites,
+                     int32_t nsites, int32_t r_max, int32_t dtype, void* stream) {
+    return finish(lora_apply(meta, x, ldx, m, sites, nsites, r_max, dtype, static_cast<cudaStream_t>(stream),
+                             current_num_sms()));
+}
+
+int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t ldh, int32_t d, const void* A, const void* B,
+                     const void* bias, const void* scale, int32_t r_max, int32_t dtype, void* stream) {
+    return finish(reft_apply(meta, h, ldh, d, A, B, bias, scale, r_max, dtype, static_cast<cudaStream_t>(stream),
+                             current_num_sms()));
+}
+
+int preft_convert_2d(void* dst, int32_t dst_dtype, int64_t dst_ld, const double* src, int64_t src_stride_row,
+                     int64_t src_stride_col, int64_t rows_valid, int64_t rows, int64_t cols, void* stream) {
+    if (!dst || (!src && rows_valid > 0) || rows < 0 || cols < 0 || rows_valid < 0 || rows_valid > rows ||
+        dst_ld < cols)
+        return PREFT_ERR_SHAPE;
+    if (rows == 0 || cols == 0) return PREFT_OK;
+    const long long total = rows * cols;
+    const int threads = 256;
+    const int grid = static_cast<int>(min(static_cast<long long>(current_num_sms()) * 8, (total + threads - 1) / threads));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (dst_dtype == PREFT_DTYPE_BF16)
+        convert_2d_kernel<__nv_bfloat16><<<grid, threads, 0, s>>>(static_cast<__nv_bfloat16*>(dst), dst_ld, src,
+                                                                  src_stride_row, src_stride_col, rows_valid, rows, cols);
+    else if (dst_dtype == PREFT_DTYPE_F32)
+        convert_2d_kernel<float><<<grid, threads, 0, s>>>(static_cast<float*>(dst), dst_ld, src, src_stride_row,
+                                                          src_stride_col, rows_valid, rows, cols);
+    else if (dst_dtype == PREFT_DTYPE_F64)
+        convert_2d_kernel<double><<<grid, threads, 0, s>>>(static_cast<double*>(dst), dst_ld, src, src_stride_row,
+                                                           src_stride_col, rows_valid, rows, cols);
+    else
+        return PREFT_ERR_DOMAIN;
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PREFT_OK : record_cuda(e);
+}
+
+}  // extern "C"

@@ -1,0 +1,222 @@
+// K3 — fused ReFT^P residual edit for sm_100a (SIMT path, rank <= 64).
+//
+// For every selected token t (adapter slot a):
+//
+//     h[t, :] += scale[a] * ((h[t, :] . A[a]^T + b[a]) . B[a])
+//
+//   DiReFT: A, B, b exactly as the reference stores them       (adapters.py:292-293)
+//   LoReFT: A := W - R (folded in f64 at registration), B := R  (adapters.py:294-295)
+//
+// One warp per token row.  When the row fits in registers (KEEP vectors per
+// lane, e.g. d = 4096 in bf16 -> 16 x 128-bit per lane) it is loaded once,
+// used for the shrink and updated in registers for the expand, so h moves
+// HBM->SM->HBM exactly once — the algorithmic minimum 2*d*e bytes per token.
+// Wider rows re-read h for the expand (an L1/L2 hit in practice).
+#include "common.cuh"
+
+namespace preft {
+
+struct ReftArgs {
+    void* h;
+    long long ldh;
+    int d;
+    int slot_base;
+    const void* A;
+    const void* B;
+    const void* bias;
+    const void* scale;
+    const int2* tokens;
+    const int* counters;
+};
+
+template <typename T, bool VEC, int R, int U, int KEEP>
+__global__ void __launch_bounds__(256) reft_kernel(const ReftArgs a) {
+    using V = Vec<T, VEC>;
+    using acc_t = typename V::acc_t;
+    constexpr int W = V::W;
+    const int lane = threadIdx.x & 31;
+    const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    // ReFT-class tokens: sorted positions [split, n_selected), slots >= slot_base
+    const int lo = a.counters[PREFT_CTR_SPLIT];
+    int i0, i1;
+    even_share(a.counters[PREFT_CTR_SEL_TOKENS] - lo, gw, nw, i0, i1);
+    const int dv = a.d / W;
+    const long long d = a.d;
+
+    for (int i = lo + i0; i < lo + i1; ++i) {
+        int2 ts = a.tokens[i];
+        ts.y -= a.slot_base;
+        T* __restrict__ hr = static_cast<T*>(a.h) + static_cast<long long>(ts.x) * a.ldh;
+        const T* As = static_cast<const T*>(a.A) + (static_cast<long long>(ts.y) * R) * d;
+        const T* Bs = static_cast<const T*>(a.B) + (static_cast<long long>(ts.y) * R) * d;
+        const acc_t sc = __ldg(static_cast<const acc_t*>(a.scale) + ts.y);
+        const acc_t* bb = static_cast<const acc_t*>(a.bias) + static_cast<long long>(ts.y) * R;
+
+        acc_t acc[R];
+#pragma unroll
+        for (int k = 0; k < R; ++k) acc[k] = acc_t(0);
+
+        if constexpr (KEEP > 0) {
+            // whole row resident in registers: dv <= 32 * KEEP (checked by the host)
+            typename V::raw_t hv[KEEP];
+#pragma unroll
+            for (int u = 0; u < KEEP; ++u) {
+                const int c = lane + kWarp * u;
+                hv[u] = c < dv ? V::ld_rw(hr + static_cast<long long>(c) * W) : V::zero();
+            }
+#pragma unroll
+            for (int u = 0; u < KEEP; ++u) {
+                const int c = lane + kWarp * u;
+                if (c < dv) {
+                    acc_t hf[W];
+                    V::to_acc(hv[u], hf);
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        acc_t af[W];
+                        V::to_acc(V::ld_weight(As + k * d + static_cast<long long>(c) * W), af);
+#pragma unroll
+                        for (int j = 0; j < W; ++j) acc[k] = macc(hf[j], af[j], acc[k]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc[k] = (warp_sum(acc[k]) + __ldg(bb + k)) * sc;
+#pragma unroll
+            for (int u = 0; u < KEEP; ++u) {
+                const int c = lane + kWarp * u;
+                if (c < dv) {
+                    acc_t hf[W], dl[W];
+                    V::to_acc(hv[u], hf);
+#pragma unroll
+                    for (int j = 0; j < W; ++j) dl[j] = acc_t(0);
+#pragma unroll
+                    for (int k = 0; k < R; ++k) {
+                        acc_t bf[W];
+                        V::to_acc(V::ld_weight(Bs + k * d + static_cast<long long>(c) * W), bf);
+#pragma unroll
+                        for (int j = 0; j < W; ++j) dl[j] = macc(acc[k], bf[j], dl[j]);
+                    }
+#pragma unroll
+                    for (int j = 0; j < W; ++j) hf[j] += dl[j];
+                    V::st(hr + static_cast<long long>(c) * W, hf);
+                }
+            }
+        } else {
+            for (int c0 = lane; c0 < dv; c0 += kWarp * U) {
+                typename V::raw_t hv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = c0 + kWarp * u;
+                    hv[u] = c < dv ? V::ld_rw(hr + static_cast<long long>(c) * W) : V::zero();
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = c0 + kWarp * u;
+                    if (c < dv) {
+                        acc_t hf[W];
+                        V::to_acc(hv[u], hf);
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            acc_t af[W];
+                            V::to_acc(V::ld_weight(As + k * d + static_cast<long long>(c) * W), af);
+#pragma unroll
+                            for (int j = 0; j < W; ++j) acc[k] = macc(hf[j], af[j], acc[k]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc[k] = (warp_sum(acc[k]) + __ldg(bb + k)) * sc;
+            for (int c0 = lane; c0 < dv; c0 += kWarp * U) {
+                typename V::raw_t hv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = c0 + kWarp * u;
+                    hv[u] = c < dv ? V::ld_rw(hr + static_cast<long long>(c) * W) : V::zero();
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = c0 + kWarp * u;
+                    if (c < dv) {
+                        acc_t hf[W], dl[W];
+                        V::to_acc(hv[u], hf);
+#pragma unroll
+                        for (int j = 0; j < W; ++j) dl[j] = acc_t(0);
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            acc_t bf[W];
+                            V::to_acc(V::ld_weight(Bs + k * d + static_cast<long long>(c) * W), bf);
+#pragma unroll
+                            for (int j = 0; j < W; ++j) dl[j] = macc(acc[k], bf[j], dl[j]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < W; ++j) hf[j] += dl[j];
+                        V::st(hr + static_cast<long long>(c) * W, hf);
+                    }
+                }
+            }
+        }
+    }
+}
+
+using ReftFn = void (*)(ReftArgs);
+
+template <typename T, bool VEC, int KEEP>
+ReftFn pick_reft_rank(int r) {
+    constexpr int U = VEC ? 8 : 4;
+    switch (r) {
+        case 1: return reft_kernel<T, VEC, 1, U, KEEP>;
+        case 2: return reft_kernel<T, VEC, 2, U, KEEP>;
+        case 4: return reft_kernel<T, VEC, 4, U, KEEP>;
+        case 8: return reft_kernel<T, VEC, 8, U, KEEP>;
+        case 16: return reft_kernel<T, VEC, 16, U, KEEP>;
+        case 32: return reft_kernel<T, VEC, 32, U, KEEP>;
+        case 64: if constexpr (KEEP == 0) return reft_kernel<T, VEC, 64, 4, 0>; else return nullptr;
+        default: return nullptr;
+    }
+}
+
+static bool aligned16r(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+int grid_for(const void* fn, int threads, int num_sms);
+
+int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
+               const void* bias, const void* scale, int r, int dtype, cudaStream_t stream, int num_sms) {
+    if (!meta || !h || !A || !B || !bias || !scale || d < 1 || ldh < d) return PREFT_ERR_SHAPE;
+    if (r < 1 || r > 64 || (r & (r - 1))) return PREFT_ERR_RANK;
+    if (dtype != PREFT_DTYPE_F32 && dtype != PREFT_DTYPE_BF16 && dtype != PREFT_DTYPE_F64) return PREFT_ERR_DOMAIN;
+    const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;
+    const bool vec = (d % W == 0) && (ldh % W == 0) && aligned16r(h) && aligned16r(A) && aligned16r(B);
+    const int dv = vec ? d / W : d;
+    ReftArgs args{};
+    args.h = h;
+    args.ldh = ldh;
+    args.d = d;
+    args.slot_base = meta->slot_split;
+    args.A = A;
+    args.B = B;
+    args.bias = bias;
+    args.scale = scale;
+    args.tokens = reinterpret_cast<const int2*>(meta->tokens);
+    args.counters = meta->counters;
+    ReftFn fn = nullptr;
+    if (dtype == PREFT_DTYPE_BF16) {
+        if (vec && dv <= 32 * 16 && r <= 32) fn = pick_reft_rank<__nv_bfloat16, true, 16>(r);
+        else if (vec) fn = pick_reft_rank<__nv_bfloat16, true, 0>(r);
+        else fn = pick_reft_rank<__nv_bfloat16, false, 0>(r);
+    } else if (dtype == PREFT_DTYPE_F32) {
+        if (vec && dv <= 32 * 8 && r <= 32) fn = pick_reft_rank<float, true, 8>(r);
+        else if (vec) fn = pick_reft_rank<float, true, 0>(r);
+        else fn = pick_reft_rank<float, false, 0>(r);
+    } else {
+        fn = vec ? pick_reft_rank<double, true, 0>(r) : pick_reft_rank<double, false, 0>(r);
+    }
+    if (!fn) return PREFT_ERR_RANK;
+    const int grid = grid_for(reinterpret_cast<const void*>(fn), 256, num_sms);
+    fn<<<grid, 256, 0, stream>>>(args);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PREFT_OK : -static_cast<int>(e);
+}
+
+}  // namespace preft

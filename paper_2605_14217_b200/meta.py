@@ -1,0 +1,202 @@
+"""Device batch metadata (K1) — the B200 replacement for compute_position_mask
+and the per-entry row selection of forward_chunk (model.py:305-319, 474-475,
+509, 538).
+
+`BatchMeta` owns a fixed-capacity, fixed-address device workspace (so the
+step that uses it can be captured in a CUDA graph) plus a pinned host staging
+buffer.  Per step the host packs (E, T, query_start_loc, slot, flags) into the
+pinned buffer, issues ONE async H2D copy and launches `preft_meta_build`; the
+kernels after it read everything they need (selected-token count, sorted
+(token, slot) list, tiles) from device memory, so there is no host sync on
+the hot path.  Reading results back (`mask_host`, `counters_host`, ...) is for
+tests and the reference-shaped API only.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Mapping
+
+import numpy as np
+import torch
+
+from . import _lib
+from .adapters import PositionSchedule
+from .batch import ForwardBatch, Phase, mask_uniform
+from .errors import BatchError, InfeasibleBatchError
+
+__all__ = ["BatchMeta", "default_meta", "pack_entries"]
+
+
+def pack_entries(batch: ForwardBatch, slot_of: Mapping[int, int]) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """(query_start_loc int32[E+1], slot int32[E], flags int32[E]) for K1.
+
+    An entry whose adapter is not registered raises BatchError, as
+    forward_chunk does for ids missing from the catalogue (model.py:470-472).
+    """
+    E = len(batch.entries)
+    qsl = np.asarray(batch.query_start_loc, dtype=np.int32)
+    slots = np.full(E, -1, dtype=np.int32)
+    flags = np.zeros(E, dtype=np.int32)
+    for i, e in enumerate(batch.entries):
+        if e.adapter_id is not None:
+            s = slot_of.get(e.adapter_id)
+            if s is None:
+                raise BatchError(f"adapter {e.adapter_id} not in catalogue")
+            slots[i] = s
+        f = 0
+        if e.phase is Phase.DECODE:
+            f |= _lib.ENTRY_DECODE
+        if e.schedule is PositionSchedule.ALL_POSITIONS:
+            f |= _lib.ENTRY_ALL_POSITIONS
+        flags[i] = f
+    return qsl, slots, flags
+
+
+class BatchMeta:
+    """Fixed-capacity device workspace for one in-flight step."""
+
+    def __init__(self, max_entries: int, max_tokens: int, tile_tokens: int = 16, device=None):
+        if not 1 <= max_entries <= _lib.MAX_ENTRIES:
+            raise InfeasibleBatchError(f"max_entries must be in [1, {_lib.MAX_ENTRIES}], got {max_entries}")
+        if max_tokens < 1 or tile_tokens < 1:
+            raise InfeasibleBatchError("max_tokens and tile_tokens must be >= 1")
+        self.device = _lib.require_cuda(device)
+        lib = _lib.load()
+        self.E_cap = int(max_entries)
+        self.T_cap = int(max_tokens)
+        self.tile_tokens = int(tile_tokens)
+        self.tile_cap = self.E_cap + self.T_cap // self.tile_tokens + 1
+        words = int(lib.preft_meta_entries_words(self.E_cap))
+        i32 = dict(dtype=torch.int32, device=self.device)
+        self.entries = torch.zeros(words, **i32)
+        self.mask = torch.zeros(self.T_cap, dtype=torch.uint8, device=self.device)
+        self.tokens = torch.zeros(2 * self.T_cap, **i32)
+        self.segments = torch.zeros(3 * self.E_cap, **i32)
+        self.tiles = torch.zeros(4 * self.tile_cap, **i32)
+        self.entry_offset = torch.zeros(self.E_cap, **i32)
+        self.counters = torch.zeros(_lib.NUM_COUNTERS, **i32)
+        self.host = torch.zeros(words, dtype=torch.int32, pin_memory=True)
+        self._host_np = self.host.numpy()
+        self._staged = None  # event: the last H2D from `host` has been consumed
+        self.c = _lib.PreftMeta(
+            self.entries.data_ptr(),
+            self.mask.data_ptr(),
+            self.tokens.data_ptr(),
+            self.segments.data_ptr(),
+            self.tiles.data_ptr(),
+            self.entry_offset.data_ptr(),
+            self.counters.data_ptr(),
+            self.E_cap,
+            self.T_cap,
+            self.tile_cap,
+            self.tile_tokens,
+            _lib.SLOT_SPLIT_ALL_LORA,
+            0,
+        )
+        self.E = 0
+        self.T = 0
+        self.uniform: bool | None = None
+
+    @property
+    def h2d_bytes(self) -> int:
+        return 4 * (2 + (self.E + 1) + 2 * self.E)
+
+    def fits(self, n_entries: int, n_tokens: int) -> bool:
+        return n_entries <= self.E_cap and n_tokens <= self.T_cap
+
+    # ------------------------------------------------------------ build
+    def build(self, batch: ForwardBatch, slot_of: Mapping[int, int], stream: torch.cuda.Stream | None = None):
+        """Stage a ForwardBatch and launch K1 on `stream` (default: current)."""
+        qsl, slots, flags = pack_entries(batch, slot_of)
+        self.uniform = mask_uniform(batch)
+        return self.build_arrays(qsl, slots, flags, stream)
+
+    def set_slot_split(self, split: int) -> None:
+        """First ReFT-class slot (AdapterPool.slot_split); LoRA slots lie below it."""
+        self.c.slot_split = int(split)
+
+    def build_arrays(self, qsl: np.ndarray, slots: np.ndarray, flags: np.ndarray, stream=None):
+        """Stage raw int32 arrays (qsl[E+1], slot[E], flags[E]) and launch K1."""
+        E = int(len(slots))
+        T = int(qsl[-1]) if E else 0
+        if E < 1:
+            raise BatchError("batch must contain at least one entry")
+        if not self.fits(E, T):
+            raise InfeasibleBatchError(
+                f"batch of {E} entries / {T} tokens exceeds the workspace ({self.E_cap} / {self.T_cap})"
+            )
+        if self._staged is not None:
+            self._staged.synchronize()  # never overwrite a pinned buffer still being copied
+        h = self._host_np
+        h[0] = E
+        h[1] = T
+        h[2 : 3 + E] = qsl
+        h[3 + E : 3 + 2 * E] = slots
+        h[3 + 2 * E : 3 + 3 * E] = flags
+        n = 3 + 3 * E
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(s):
+            self.entries[:n].copy_(self.host[:n], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(s)
+            self._staged = ev
+        _lib.check(_lib.load().preft_meta_build(ctypes.byref(self.c), ctypes.c_void_p(s.cuda_stream)), "meta_build")
+        self.E, self.T = E, T
+        return self
+
+    def launch(self, stream=None):
+        """Re-run K1 on whatever is in `entries` (graph replay helper)."""
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        _lib.check(_lib.load().preft_meta_build(ctypes.byref(self.c), ctypes.c_void_p(s.cuda_stream)), "meta_build")
+
+    # ------------------------------------------------------------ readback (syncs)
+    def counters_host(self) -> np.ndarray:
+        return self.counters.cpu().numpy()
+
+    def check_errors(self) -> None:
+        err = int(self.counters_host()[_lib.CTR_ERR])
+        if err & (_lib.META_ERR_E_RANGE | _lib.META_ERR_T_RANGE | _lib.META_ERR_QSL):
+            raise BatchError(f"device rejected the batch metadata (error bits {err:#x})")
+        if err & _lib.META_ERR_TILES:
+            raise InfeasibleBatchError("work list exceeded the tile capacity")
+
+    def mask_host(self) -> np.ndarray:
+        self.check_errors()
+        return self.mask[: self.T].cpu().numpy().astype(bool)
+
+    def selected_tokens(self) -> int:
+        return int(self.counters_host()[_lib.CTR_SEL_TOKENS])
+
+    def tokens_host(self) -> np.ndarray:
+        n = self.selected_tokens()
+        return self.tokens[: 2 * n].view(n, 2).cpu().numpy()
+
+    def segments_host(self) -> np.ndarray:
+        n = int(self.counters_host()[_lib.CTR_SEGMENTS])
+        return self.segments[: 3 * n].view(n, 3).cpu().numpy()
+
+    def tiles_host(self) -> np.ndarray:
+        n = int(self.counters_host()[_lib.CTR_TILES])
+        return self.tiles[: 4 * n].view(n, 4).cpu().numpy()
+
+    def entry_offset_host(self) -> np.ndarray:
+        return self.entry_offset[: self.E].cpu().numpy()
+
+
+_DEFAULT: dict[int, BatchMeta] = {}
+
+
+def default_meta(n_entries: int, n_tokens: int, device=None) -> BatchMeta:
+    """Per-device scratch workspace for the reference-shaped API (grows as needed)."""
+    dev = _lib.require_cuda(device)
+    idx = dev.index if dev.index is not None else torch.cuda.current_device()
+    cur = _DEFAULT.get(idx)
+    if cur is None or not cur.fits(n_entries, n_tokens):
+        E = max(n_entries, 64 if cur is None else cur.E_cap)
+        T = max(n_tokens, 4096 if cur is None else cur.T_cap)
+        if E > _lib.MAX_ENTRIES:
+            raise InfeasibleBatchError(f"{n_entries} entries exceed the device limit {_lib.MAX_ENTRIES}")
+        cur = BatchMeta(min(_lib.MAX_ENTRIES, max(E, 1)), T, device=torch.device("cuda", idx))
+        _DEFAULT[idx] = cur
+    return cur

@@ -1,0 +1,118 @@
+"""StepPlan — one native call per step for the whole hot path.
+
+The reference runs its adapter hooks inside a Python `layer x entry` loop
+(model.py:504-546).  A StepPlan records, once, every launch a step needs
+(K1 + one fused launch per LoRA site group or ReFT site per layer, all with
+fixed pointers into the pool and the activation buffers) in the native
+executor (csrc/plan.cu); `run()` then issues the step with a single C call.
+The plan is CUDA-graph capturable (`capture()`), which removes the host from
+the loop entirely for small, launch-bound batches.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .errors import ShapeError
+from .meta import BatchMeta
+from .ops import _check_act, row_stride
+from .pool import AdapterPool
+
+__all__ = ["StepPlan"]
+
+
+class StepPlan:
+    def __init__(self, meta: BatchMeta, pool: AdapterPool, max_tokens: int | None = None):
+        self.lib = _lib.load()
+        self.meta = meta
+        self.pool = pool
+        self.rows = max_tokens if max_tokens is not None else meta.T_cap
+        meta.set_slot_split(pool.slot_split)
+        self.handle = self.lib.preft_plan_create(ctypes.byref(meta.c))
+        if not self.handle:
+            raise ShapeError("could not create a step plan")
+        self.lib.preft_plan_set_slot_split(self.handle, pool.slot_split)
+        self._keep: list = []  # tensors the plan points into
+        self.n_ops = 0
+        self.graph: torch.cuda.CUDAGraph | None = None
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h:
+            self.lib.preft_plan_destroy(h)
+            self.handle = None
+
+    def add_lora_group(self, ys: Sequence[torch.Tensor], x: torch.Tensor, layer: int, sites: Sequence[str],
+                       tag: int = -1) -> None:
+        pool = self.pool
+        if not 1 <= len(sites) <= 3 or len(ys) != len(sites):
+            raise ShapeError("a LoRA group has 1 to 3 sites and one output per site")
+        m = pool.lora_sites[sites[0]][1]
+        if any(pool.lora_sites[s][1] != m for s in sites):
+            raise ShapeError(f"sites {tuple(sites)} do not share an input width")
+        _check_act(x, "x", m, self.rows, pool.dtype, pool.device)
+        arr = (_lib.PreftLoraSite * 3)()
+        for i, (name, y) in enumerate(zip(sites, ys)):
+            n = pool.lora_sites[name][0]
+            _check_act(y, f"y[{name}]", n, self.rows, pool.dtype, pool.device)
+            arr[i].A = pool.lora_A[name][layer].data_ptr()
+            arr[i].Bt = pool.lora_Bt[name][layer].data_ptr()
+            arr[i].scale = pool.lora_scale[name][layer].data_ptr()
+            arr[i].bias = None
+            arr[i].y = y.data_ptr()
+            arr[i].ldy = row_stride(y)
+            arr[i].n = n
+        st = self.lib.preft_plan_add_lora(self.handle, ctypes.c_void_p(x.data_ptr()), row_stride(x), m, arr,
+                                          len(sites), pool.lora_rank, pool.dtype_code, tag)
+        _lib.check(st, "plan_add_lora")
+        self._keep += [x, *ys]
+        self.n_ops += 1
+
+    def add_reft(self, h: torch.Tensor, layer: int, tag: int = -1) -> None:
+        pool = self.pool
+        _check_act(h, "h", pool.d_model, self.rows, pool.dtype, pool.device)
+        st = self.lib.preft_plan_add_reft(
+            self.handle, ctypes.c_void_p(h.data_ptr()), row_stride(h), pool.d_model,
+            ctypes.c_void_p(pool.reft_A[layer].data_ptr()), ctypes.c_void_p(pool.reft_B[layer].data_ptr()),
+            ctypes.c_void_p(pool.reft_bias[layer].data_ptr()), ctypes.c_void_p(pool.reft_scale[layer].data_ptr()),
+            pool.reft_rank, pool.dtype_code, tag
+        )
+        _lib.check(st, "plan_add_reft")
+        self._keep.append(h)
+        self.n_ops += 1
+
+    @property
+    def launches_per_run(self) -> int:
+        """Kernels one run() launches: K1 (2) + one per op."""
+        return 2 + self.n_ops
+
+    def set_timing(self, tag: int, reserve_pairs: int) -> None:
+        _lib.check(self.lib.preft_plan_set_timing(self.handle, tag, reserve_pairs), "plan_set_timing")
+
+    def collect_timing(self) -> tuple[float, int]:
+        total = ctypes.c_double(0.0)
+        count = ctypes.c_int32(0)
+        _lib.check(self.lib.preft_plan_collect_timing(self.handle, ctypes.byref(total), ctypes.byref(count)),
+                   "plan_collect_timing")
+        return total.value, count.value
+
+    def run(self, stream=None, run_meta: bool = True) -> None:
+        s = stream if stream is not None else torch.cuda.current_stream(self.pool.device)
+        _lib.check(self.lib.preft_plan_run(self.handle, int(run_meta), ctypes.c_void_p(s.cuda_stream)), "plan_run")
+
+    def capture(self, stream=None) -> torch.cuda.CUDAGraph:
+        """Capture one run() into a CUDA graph (timing must be off)."""
+        s = stream if stream is not None else torch.cuda.Stream(self.pool.device)
+        s.wait_stream(torch.cuda.current_stream(self.pool.device))
+        with torch.cuda.stream(s):
+            self.run(s)  # warm-up: occupancy queries, smem attributes
+        torch.cuda.current_stream(self.pool.device).wait_stream(s)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            self.run(s)
+        self.graph = g
+        return g

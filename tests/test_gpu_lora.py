@@ -1,0 +1,191 @@
+"""K2 (fused LoRA^P) vs the oracle and the reference's golden outputs."""
+
+import numpy as np
+import pytest
+import torch
+
+import gpu_util as U
+import helpers
+from paper_2605_14217_b200 import AdapterKind, AdapterParams, ModelAdapter, PositionSchedule, ScalingRule
+from paper_2605_14217_b200.errors import BatchError, ShapeError
+
+pytestmark = pytest.mark.gpu
+
+MODES = {"f64": torch.float64, "f32": torch.float32, "bf16": torch.bfloat16}
+
+
+def _golden_pool(g, dtype, device):
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    d = int(g["d"])
+    pool = AdapterPool(1, d, lora_sites={"Wq": (d, d)}, lora_capacity=4, lora_rank=1, reft_capacity=5, reft_rank=8,
+                       dtype=dtype, device=device)
+    for aid in range(9):
+        kind = AdapterKind(str(g[f"a{aid}_kind"]))
+        rank = int(g[f"a{aid}_rank"])
+        kw = {k: g[f"a{aid}_{k}"] for k in ("A", "B", "b", "R", "W") if f"a{aid}_{k}" in g.files}
+        dims = (d, d) if kind is AdapterKind.LORA else (d,)
+        p = AdapterParams(kind, rank, dims, ScalingRule.constant(float(g[f"a{aid}_s"])), **kw)
+        if kind is AdapterKind.LORA:
+            pool.register(ModelAdapter(aid, kind, rank, PositionSchedule.PREFILL_ONLY, lora_sites={(0, "Wq"): p}))
+        else:
+            pool.register(ModelAdapter(aid, kind, rank, PositionSchedule.PREFILL_ONLY, reft_sites=(p,)))
+    return pool
+
+
+@pytest.mark.parametrize("name", ["hooks_config1_small.npz", "hooks_config1_small_shuffled.npz"])
+@pytest.mark.parametrize("mode", ["f64", "f32", "bf16"])
+def test_config1_small_against_reference(cuda_device, name, mode):
+    """Reduced BASELINE config 1 (mixed LoRA^P r=1 + DiReFT^P r=8 + LoReFT^P,
+    decode entries first or shuffled) through both hook kernels."""
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_, apply_reft_
+
+    g = helpers.load(name)
+    dtype = MODES[mode]
+    pool = _golden_pool(g, dtype, cuda_device)
+    meta = BatchMeta(64, 4096, device=cuda_device)
+    qsl = g["qsl"].astype(np.int32)
+    ids = [None if a < 0 else int(a) for a in g["adapter"]]
+    flags = (g["is_decode"].astype(np.int32) * 1 | g["all_pos"].astype(np.int32) * 2).astype(np.int32)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    assert np.array_equal(meta.mask_host(), g["mask"])
+
+    x = torch.from_numpy(g["x"]).to(cuda_device, dtype)
+    y = torch.from_numpy(g["y_base"]).to(cuda_device, dtype)
+    h = torch.from_numpy(g["h"]).to(cuda_device, dtype)
+    y_in, h_in = U.to_np(y), U.to_np(h)
+    apply_lora_(y, x, meta, pool, 0, "Wq")
+    apply_reft_(h, meta, pool, 0)
+    y_out, h_out = U.to_np(y), U.to_np(h)
+    mask = g["mask"]
+    # untouched rows are bit-identical (tests/test_model.py:298-327 contract)
+    assert np.array_equal(y_out[~mask], y_in[~mask])
+    assert np.array_equal(h_out[~mask], h_in[~mask])
+    if mode == "f64":
+        helpers.check_close(y_out, y_in, g["y_ref"], "f64", "lora vs reference")
+        helpers.check_close(h_out, h_in, g["h_ref"], "f64", "reft vs reference")
+    # oracle on the exact (quantised) device inputs
+    y_ref = U.lora_oracle(y_in, U.to_np(x), qsl, slots, flags, pool, 0, "Wq")
+    h_ref = U.reft_oracle(h_in, qsl, slots, flags, pool, 0)
+    helpers.check_close(y_out, y_in, y_ref, mode, "lora vs oracle")
+    helpers.check_close(h_out, h_in, h_ref, mode, "reft vs oracle")
+
+
+SITES = {"Wq": (256, 128), "Wk": (64, 128), "Wv": (64, 128), "Wo": (128, 256)}
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16", "f64"])
+@pytest.mark.parametrize("rank", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("group", [("Wq",), ("Wq", "Wk"), ("Wq", "Wk", "Wv"), ("Wo",)])
+def test_random_batches_groups_ranks(cuda_device, mode, rank, group):
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_group_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    if len(group) * rank > 64:
+        pytest.skip("group x rank above the fused limit")
+    rng = np.random.default_rng(rank * 7 + len(group))
+    dtype = MODES[mode]
+    pool = AdapterPool(2, 128, lora_sites=SITES, lora_capacity=12, lora_rank=rank, dtype=dtype, device=cuda_device)
+    for aid in range(10):
+        r = rank if aid % 3 else max(1, rank // 2)  # mixed ranks in one pool
+        pool.register(U.random_lora_adapter(rng, 100 + aid, 2, SITES, r))
+    meta = BatchMeta(256, 8192, device=cuda_device)
+    qsl, ids, flags = U.random_entries(rng, 120, [100 + a for a in range(10)], max_len=50)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    T = int(qsl[-1])
+    m = SITES[group[0]][1]
+    x = U.rand_act(rng, T, m, dtype, cuda_device)
+    ys = [U.rand_act(rng, T, SITES[s][0], dtype, cuda_device) for s in group]
+    y_in = [U.to_np(y) for y in ys]
+    layer = 1
+    apply_lora_group_(ys, x, meta, pool, layer, group)
+    mask = U.oracle_mask(qsl, slots, flags)
+    for s, y, yi in zip(group, ys, y_in):
+        out = U.to_np(y)
+        assert np.array_equal(out[~mask], yi[~mask])
+        ref = U.lora_oracle(yi, U.to_np(x), qsl, slots, flags, pool, layer, s)
+        helpers.check_close(out, yi, ref, mode, f"{s} r={rank}")
+
+
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+def test_odd_widths_use_scalar_path(cuda_device, mode):
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_group_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    sites = {"Wgate": (45, 37), "Wup": (45, 37)}
+    rng = np.random.default_rng(5)
+    dtype = MODES[mode]
+    pool = AdapterPool(1, 37, lora_sites=sites, lora_capacity=4, lora_rank=4, dtype=dtype, device=cuda_device)
+    for aid in range(4):
+        pool.register(U.random_lora_adapter(rng, aid, 1, sites, 3))
+    meta = BatchMeta(64, 4096, device=cuda_device)
+    qsl, ids, flags = U.random_entries(rng, 30, list(range(4)))
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    T = int(qsl[-1])
+    x = U.rand_act(rng, T, 37, dtype, cuda_device)
+    ys = [U.rand_act(rng, T, 45, dtype, cuda_device) for _ in sites]
+    y_in = [U.to_np(y) for y in ys]
+    apply_lora_group_(ys, x, meta, pool, 0, tuple(sites))
+    for s, y, yi in zip(sites, ys, y_in):
+        ref = U.lora_oracle(yi, U.to_np(x), qsl, slots, flags, pool, 0, s)
+        helpers.check_close(U.to_np(y), yi, ref, mode, s)
+
+
+def test_llama8b_shapes_sampled_parity(cuda_device):
+    """Full Llama-3.1-8B site widths (one layer, 64 adapters r=1, bf16):
+    every unselected row bit-identical; a sample of selected rows against
+    the oracle on the device's own values."""
+    from paper_2605_14217_b200 import shapes
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_group_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(8)
+    sites = shapes.LLAMA_8B.site_dims()
+    pool = AdapterPool(1, 4096, lora_sites=sites, lora_capacity=64, lora_rank=1, dtype=torch.bfloat16,
+                       device=cuda_device)
+    ids = pool.fill_synthetic_(64, AdapterKind.LORA, 1, seed=3)
+    meta = BatchMeta(256, 16384, device=cuda_device)
+    qsl, eids, flags = U.random_entries(rng, 96, ids, max_len=64)
+    slots = U.stage(meta, pool, qsl, eids, flags)
+    T = int(qsl[-1])
+    mask = U.oracle_mask(qsl, slots, flags)
+    for group in (("Wq", "Wk", "Wv"), ("Wo",), ("Wgate", "Wup"), ("Wdown",)):
+        m = sites[group[0]][1]
+        x = U.rand_act(rng, T, m, torch.bfloat16, cuda_device)
+        ys = [U.rand_act(rng, T, sites[s][0], torch.bfloat16, cuda_device) for s in group]
+        y_in = [y.clone() for y in ys]
+        apply_lora_group_(ys, x, meta, pool, 0, group)
+        sample = rng.choice(np.flatnonzero(mask), size=min(24, int(mask.sum())), replace=False)
+        keep = np.zeros(T, bool)
+        keep[sample] = True
+        for s, y, yi in zip(group, ys, y_in):
+            assert torch.equal(y[torch.from_numpy(~mask).to(cuda_device)], yi[torch.from_numpy(~mask).to(cuda_device)])
+            # oracle on the sampled rows only (other rows masked out of the check)
+            yi_np, x_np, out = U.to_np(yi), U.to_np(x), U.to_np(y)
+            sub_mask_flags = flags.copy()
+            ref = U.lora_oracle(yi_np, x_np, qsl, slots, flags, pool, 0, s)
+            helpers.check_close(out[keep], yi_np[keep], ref[keep], "bf16", f"8B {s}")
+
+
+def test_errors_map_to_reference_exceptions(cuda_device):
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    pool = AdapterPool(1, 64, lora_sites={"Wq": (64, 64)}, lora_capacity=2, lora_rank=2, dtype=torch.float32,
+                       device=cuda_device)
+    meta = BatchMeta(8, 64, device=cuda_device)
+    with pytest.raises(BatchError):  # unknown adapter id (model.py:470-472)
+        U.stage(meta, pool, np.array([0, 3], np.int32), [5], np.zeros(1, np.int32))
+    U.stage(meta, pool, np.array([0, 3], np.int32), [None], np.zeros(1, np.int32))
+    x = torch.zeros(3, 64, device=cuda_device)
+    with pytest.raises(ShapeError):
+        apply_lora_(torch.zeros(3, 32, device=cuda_device), x, meta, pool, 0, "Wq")
+    with pytest.raises(ShapeError):
+        apply_lora_(torch.zeros(3, 64, device=cuda_device, dtype=torch.bfloat16), x, meta, pool, 0, "Wq")
+    with pytest.raises(ShapeError):
+        apply_lora_(torch.zeros(2, 64, device=cuda_device), x, meta, pool, 0, "Wq")
