@@ -1,0 +1,575 @@
+#!/usr/bin/env python
+"""bench.py — PreFT hot path on B200: prefill adapter tokens/s @512 adapters
+(Llama-3.1-8B shapes) and % of HBM roofline.
+
+Workload (BASELINE.json configs[1], "cfg2"): Llama-3.1-8B projection shapes,
+32 layers x 7 LoRA^P sites (q/k/v, o, gate/up, down; sites that share an
+input run as one fused launch), 512 LoRA^P rank-1 adapters (A, B ~ N(0,
+0.01^2)) held in the HBM pool, Uniform Punica batch:
+per GPU 256 prefill requests with Punica prompt lengths (lognormal, mean
+~24, workload.py:110-116) and adapters uniform over the GPU's adapter shard,
+plus 256 decode tokens (PREFILL_ONLY adapters -> skipped) listed first as
+the reference engine does (engine.py:618-648).
+
+One step = K1 (device metadata from the resident entry buffer) + 128 fused
+LoRA launches (4 groups x 32 layers), issued by the native step plan.
+`value` counts SELECTED prefill tokens through all 32 layers x 7 sites per
+second of device time (CUDA events, max over ranks).  `e2e` is the same
+metric through the reference-shaped host-buffer path: every step uploads the
+entries and every layer's site activations from pinned host memory and
+reads every updated output back.
+
+--impl reference times the reference's CPU implementation of the same path
+(oracle/preft_oracle.py: the float64 numpy restatement of delta_for_rows /
+the forward_chunk hooks, the reference itself being pure Python that cannot
+travel to the GPU box) on all host cores, on rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "prefill adapter tokens/s @512 adapters (Llama-3.1-8B shapes); % HBM roofline"
+UNIT = "tokens/s"
+N_ADAPTERS = 512
+RANK = 1
+N_LAYERS = 32
+SEED = 0
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--requests", type=int, default=256, help="prefill requests per GPU per step")
+    p.add_argument("--decodes", type=int, default=256, help="decode tokens per GPU per step")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-punica-step", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU baseline sample length")
+    p.add_argument("--ref-requests", type=int, default=4, help="reference arm: requests per worker per step")
+    return p.parse_args()
+
+
+# ---------------------------------------------------------------- workload
+
+
+def step_entries(rank: int, world: int, n_prefill: int, n_decode: int, seed: int = SEED):
+    """(qsl, adapter ids, flags, prompt lens) of one mixed step on one GPU.
+
+    Prompt lengths: Punica lognormal (the reference's sampler); adapters
+    uniform over the adapters this GPU owns (pool sharded by id, requests
+    routed to the owner: SURVEY.md 8(e)).  Decode entries first.
+    """
+    from paper_2605_14217_b200 import _lib
+    from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig, sample_prompt_lens, shard_adapters
+
+    owned = shard_adapters(N_ADAPTERS, rank, world)
+    cfg = WorkloadConfig(n_prefill + n_decode, N_ADAPTERS, AdapterMix.UNIFORM, seed + rank)
+    lens = sample_prompt_lens(cfg)[:n_prefill]
+    rng = np.random.default_rng(seed * 1000 + rank)
+    ids = [int(owned[i]) for i in rng.integers(0, len(owned), size=n_prefill + n_decode)]
+    all_lens = np.concatenate([np.ones(n_decode, dtype=np.int64), lens])
+    qsl = np.concatenate([[0], np.cumsum(all_lens)]).astype(np.int32)
+    flags = np.array([_lib.ENTRY_DECODE] * n_decode + [0] * n_prefill, dtype=np.int32)
+    adapter_ids = ids[n_prefill:] + ids[:n_prefill]  # decode ids, then prefill ids
+    return qsl, adapter_ids, flags, lens, owned
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = Path(tempfile.mkstemp(prefix="clocks_", suffix=".csv")[1])
+
+    def start(self):
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.3)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.fh.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.path.read_text().splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        self.path.unlink(missing_ok=True)
+        return {
+            "sm_mhz": statistics.median(sm) if sm else None,
+            "sm_max_mhz": max(mx) if mx else None,
+            "samples": len(sm),
+            "reasons": sorted(reasons),
+        }
+
+
+# ---------------------------------------------------------------- roofline helpers
+
+
+def measured_peak_gbs() -> tuple[float, str]:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return float(json.loads(p.read_text())["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        except (KeyError, ValueError):
+            pass
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def group_bytes(shape, group, n_tokens: int, distinct: int, rank: int = RANK, elem: int = 2) -> int:
+    """Algorithmic bytes of one fused launch: x read once,
+    every y read + written, each distinct adapter's A/Bt rows once."""
+    dims = shape.site_dims()
+    m = dims[group[0]][1]
+    act = n_tokens * elem * (m + 2 * sum(dims[s][0] for s in group))
+    wts = distinct * elem * rank * sum(m + dims[s][0] for s in group)
+    return act + wts
+
+
+def ncu_traffic(kernel_hint: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu summary, if any."""
+    for f in sorted((ROOT / "profiles").glob("ncu_summary_*.json"), reverse=True):
+        try:
+            d = json.loads(f.read_text())
+            v = d.get("kernels", {}).get(kernel_hint, {}).get("dram_bytes_per_launch")
+            if v:
+                return float(v), f.name
+        except (ValueError, OSError):
+            continue
+    return None, None
+
+
+# ---------------------------------------------------------------- distributed
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def dist_init(world, local):
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+def all_max(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def all_sum(value: float, world: int) -> float:
+    if world == 1:
+        return value
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- our arm
+
+
+def build_step(args, rank, world, device, n_prefill, n_decode, seed=SEED):
+    import torch
+
+    from paper_2605_14217_b200 import AdapterKind, shapes
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.plan import StepPlan
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    shape = shapes.LLAMA_8B
+    qsl, ids, flags, lens, owned = step_entries(rank, world, n_prefill, n_decode, seed)
+    pool = AdapterPool(N_LAYERS, shape.d_model, lora_sites=shape.site_dims(), lora_capacity=len(owned),
+                       lora_rank=RANK, dtype=torch.bfloat16, device=device)
+    pool.fill_synthetic_(0, AdapterKind.LORA, RANK, seed=seed + 17 * rank, sigma=0.01, ids=owned)
+    slots = pool.entry_arrays(qsl, ids, flags)
+    E, T = len(ids), int(qsl[-1])
+    meta = BatchMeta(E, T, tile_tokens=16, device=device)
+    meta.set_slot_split(pool.slot_split)
+    meta.build_arrays(qsl, slots, flags)  # entries now resident in HBM
+    dims = shape.site_dims()
+    g = torch.Generator(device=device)
+    g.manual_seed(1234 + rank)
+    acts = {}
+    for group in shapes.SITE_GROUPS:
+        m = dims[group[0]][1]
+        x = torch.randn(T, m, generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+        ys = [torch.randn(T, dims[s][0], generator=g, device=device, dtype=torch.float32).to(torch.bfloat16)
+              for s in group]
+        acts[group] = (x, ys)
+    plan = StepPlan(meta, pool, max_tokens=T)
+    for layer in range(N_LAYERS):
+        for group in shapes.SITE_GROUPS:
+            x, ys = acts[group]
+            plan.add_lora_group(ys, x, layer, group, tag=1 if group == ("Wgate", "Wup") else 0)
+    sel_prefill = int(lens.sum())
+    distinct = len({ids[i] for i in range(len(ids)) if not (flags[i] & 1)})
+    return dict(shape=shape, pool=pool, meta=meta, plan=plan, acts=acts, qsl=qsl, ids=ids, flags=flags, slots=slots,
+                lens=lens, T=T, E=E, sel=sel_prefill, distinct=distinct, owned=owned)
+
+
+def time_steps(ctx, args, world, device, timing_tag=None):
+    import torch
+
+    plan = ctx["plan"]
+    s = torch.cuda.current_stream(device)
+    for _ in range(args.warmup):
+        plan.run(s)
+    if timing_tag is not None:
+        plan.set_timing(timing_tag, args.steps * N_LAYERS + 8)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(args.steps):
+        plan.run(s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1)
+    kernel = None
+    if timing_tag is not None:
+        total, count = plan.collect_timing()
+        plan.set_timing(-1, 0)
+        kernel = (total, count)
+    return ms, kernel
+
+
+def run_e2e(ctx, args, world, device):
+    """Host-buffer path: per step H2D of the entries + every layer's site
+    activations from pinned memory, the kernels, D2H of every updated output.
+    Copies run on their own streams, double-buffered against compute."""
+    import torch
+
+    from paper_2605_14217_b200 import shapes
+    from paper_2605_14217_b200.ops import apply_lora_group_
+
+    pool, meta, T = ctx["pool"], ctx["meta"], ctx["T"]
+    dims = ctx["shape"].site_dims()
+    host_in, dev = {}, [{}, {}]
+    g = torch.Generator()
+    g.manual_seed(99)
+    h2d_bytes = d2h_bytes = 0
+    host_out = [{}, {}]
+    for group in shapes.SITE_GROUPS:
+        m = dims[group[0]][1]
+        xs = torch.randn(T, m, generator=g).to(torch.bfloat16).pin_memory()
+        ys = [torch.randn(T, dims[s][0], generator=g).to(torch.bfloat16).pin_memory() for s in group]
+        host_in[group] = (xs, ys)
+        for b in range(2):
+            dev[b][group] = (torch.empty_like(xs, device=device), [torch.empty_like(y, device=device) for y in ys])
+            host_out[b][group] = [torch.empty_like(y).pin_memory() for y in ys]
+        h2d_bytes += xs.numel() * 2 + sum(y.numel() * 2 for y in ys)
+        d2h_bytes += sum(y.numel() * 2 for y in ys)
+    comp = torch.cuda.current_stream(device)
+    up, down = torch.cuda.Stream(device), torch.cuda.Stream(device)
+    h2d_done = [torch.cuda.Event(), torch.cuda.Event()]
+    comp_done = [torch.cuda.Event(), torch.cuda.Event()]
+    d2h_done = [torch.cuda.Event(), torch.cuda.Event()]
+    qsl, slots, flags = ctx["qsl"], ctx["slots"], ctx["flags"]
+
+    def one_step():
+        meta.build_arrays(qsl, slots, flags, stream=comp)  # entries H2D + K1
+        for layer in range(N_LAYERS):
+            b = layer % 2
+            with torch.cuda.stream(up):
+                if layer >= 2:
+                    up.wait_event(d2h_done[b])
+                for group in shapes.SITE_GROUPS:
+                    xs, ys = host_in[group]
+                    xd, yds = dev[b][group]
+                    xd.copy_(xs, non_blocking=True)
+                    for yd, yh in zip(yds, ys):
+                        yd.copy_(yh, non_blocking=True)
+                h2d_done[b].record(up)
+            comp.wait_event(h2d_done[b])
+            for group in shapes.SITE_GROUPS:
+                xd, yds = dev[b][group]
+                apply_lora_group_(yds, xd, meta, pool, layer, group, stream=comp)
+            comp_done[b].record(comp)
+            with torch.cuda.stream(down):
+                down.wait_event(comp_done[b])
+                for group in shapes.SITE_GROUPS:
+                    for yh, yd in zip(host_out[b][group], dev[b][group][1]):
+                        yh.copy_(yd, non_blocking=True)
+                d2h_done[b].record(down)
+        comp.wait_stream(up)
+        comp.wait_stream(down)
+
+    for _ in range(max(1, min(args.warmup, 2))):
+        one_step()
+    torch.cuda.synchronize()
+    barrier(world)
+    n = max(2, min(args.steps, 5))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(comp)
+    for _ in range(n):
+        one_step()
+    e1.record(comp)
+    torch.cuda.synchronize()
+    barrier(world)
+    ms = e0.elapsed_time(e1) / n
+    return ms, N_LAYERS * h2d_bytes + meta.h2d_bytes, N_LAYERS * d2h_bytes, n
+
+
+def punica_step(args, rank, world, device):
+    """Secondary point: a Punica-sized step (32 prefill requests + 32 decode
+    tokens, max_batch 32, engine.py:101-112), CUDA-graph replayed."""
+    import torch
+
+    ctx = build_step(args, rank, world, device, 32, 32, seed=SEED + 7)
+    g = ctx["plan"].capture()
+    s = torch.cuda.current_stream(device)
+    for _ in range(5):
+        g.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n = 50
+    e0.record(s)
+    for _ in range(n):
+        g.replay()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    out = {"prefill_tokens": ctx["sel"], "ms_per_step": round(ms, 4),
+           "value": round(ctx["sel"] / (ms / 1e3), 1), "launch": "cuda graph"}
+    del ctx, g
+    torch.cuda.empty_cache()
+    return out
+
+
+def cpu_baseline(ctx, seconds: float) -> dict:
+    """The reference CPU path (float64 numpy oracle) on one host core, on a
+    bounded sample of the same workload: the first 8 prefill requests (plus
+    every decode entry for the mask) through 7 sites of a rotating layer."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import cpu_reference as CR
+
+    with threadpool_limits(1):
+        res = CR.time_sample(ctx["qsl"], ctx["ids"], ctx["flags"], n_requests=8, seconds=seconds, seed=SEED)
+    return {"value": round(res["tokens_per_s"], 3), "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": res["sample"]}
+
+
+def run_ours(args):
+    import torch
+
+    world, rank, local = dist_setup(args)
+    dist_init(world, local)
+    device = torch.device("cuda", local)
+    ctx = build_step(args, rank, world, device, args.requests, args.decodes)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ms_total, kernel = time_steps(ctx, args, world, device, timing_tag=1)
+    clk = clocks.stop()
+    ms_max = all_max(ms_total, world)
+    tokens_all = all_sum(ctx["sel"], world)
+    value = tokens_all * args.steps / (ms_max / 1e3)
+    peak, peak_src = measured_peak_gbs()
+    shape = ctx["shape"]
+    from paper_2605_14217_b200 import shapes
+
+    gu = ("Wgate", "Wup")
+    gu_bytes = group_bytes(shape, gu, ctx["sel"], ctx["distinct"])
+    k_ms, k_count = kernel
+    k_avg_s = (k_ms / max(k_count, 1)) / 1e3
+    achieved = gu_bytes / k_avg_s / 1e9
+    traffic, traffic_src = ncu_traffic("lora_gate_up")
+    step_bytes = N_LAYERS * sum(group_bytes(shape, gp, ctx["sel"], ctx["distinct"]) for gp in shapes.SITE_GROUPS)
+    step_s = ms_total / args.steps / 1e3
+    gpu_launches = ctx["plan"].launches_per_run * args.steps
+
+    e2e = None
+    if not args.no_e2e:
+        e_ms, bi, bo, n = run_e2e(ctx, args, world, device)
+        e_ms = all_max(e_ms, world)
+        e2e = {"value": round(tokens_all / (e_ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(bi),
+               "d2h_bytes_per_step": int(bo), "ms_per_step": round(e_ms, 3), "steps": n,
+               "path": "pinned host x/y of every layer -> device -> fused kernels -> host, copy streams overlapped"}
+    punica = None
+    if not args.no_punica_step and world == 1:
+        punica = punica_step(args, rank, world, device)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(ctx, args.cpu_seconds)
+    if rank == 0:
+        line = {
+            "metric": METRIC,
+            "value": round(value, 1),
+            "unit": UNIT,
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms_max / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (random adapters N(0,0.01^2), random bf16 activations, Punica prompt lengths)",
+            "config": {
+                "workload": "cfg2 Uniform Punica saturating step: Llama-3.1-8B shapes, 32 layers x 7 LoRA^P sites "
+                            "(4 fused groups), 512 LoRA^P r=1 adapters sharded by id, per GPU "
+                            f"{args.requests} prefill requests (Punica lengths) + {args.decodes} decode tokens",
+                "model": "Llama-3.1-8B projection shapes (GQA k/v 1024), random init",
+                "adapters": N_ADAPTERS,
+                "rank": RANK,
+                "prefill_tokens_per_gpu": ctx["sel"],
+                "tokens_per_gpu": ctx["T"],
+                "entries_per_gpu": ctx["E"],
+                "distinct_adapters_per_gpu": ctx["distinct"],
+                "global_batch": int(tokens_all),
+                "seq_len": "ragged (Punica lognormal prompts)",
+                "parallelism": f"adapter-sharded replicas x{world} (requests routed to adapter owner, no collective)",
+                "l2_policy": "inputs larger than L2: ~0.9 GB of per-layer activations stream between reuses (L2 126 MB)",
+            },
+            "roofline": {
+                "bound": "hbm",
+                "kernel": "lora_kernel<bf16,VEC,R=1,NS=2> (gate/up fused group)",
+                "achieved": round(achieved, 1),
+                "peak": peak,
+                "peak_source": peak_src,
+                "unit": "GB/s",
+                "frac": round(achieved / peak, 4),
+                "traffic": traffic,
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": gu_bytes,
+                "avg_launch_us": round(k_avg_s * 1e6, 2),
+                "launches_timed": k_count,
+                "step_frac": round(step_bytes / step_s / 1e9 / peak, 4),
+                "step_algorithmic_bytes": step_bytes,
+            },
+            "clocks": clk,
+            "gpu_launches": gpu_launches,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "punica_step": punica,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- reference arm
+
+
+def run_reference(args):
+    world, rank, local = dist_setup(args)
+    if rank != 0:
+        return  # rank 0 alone runs the CPU reference
+    from oracle import cpu_reference as CR
+
+    qsl, ids, flags, lens, owned = step_entries(0, 1, args.requests, args.decodes)
+    cores = len(os.sched_getaffinity(0))
+    res = CR.time_parallel(qsl, ids, flags, cores=cores, per_worker_requests=args.ref_requests, steps=args.steps,
+                           warmup=args.warmup, seed=SEED)
+    value = res["tokens_per_s"]
+    line = {
+        "metric": METRIC,
+        "value": round(value, 3),
+        "unit": UNIT,
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(res["ms_per_step"], 3),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic, same workload generator as the GPU arm",
+        "impl": "reference",
+        "config": {
+            "workload": "cfg2 Uniform Punica: Llama-3.1-8B shapes, 7 LoRA^P sites per layer, 512 LoRA^P r=1 adapters",
+            "model": "Llama-3.1-8B projection shapes, random init",
+            "adapters": N_ADAPTERS,
+            "rank": RANK,
+        },
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": res["sample"]},
+        "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -329,6 +329,7 @@ class AdapterPool:
         seed: int = 0,
         sigma: float = 0.01,
         first_id: int = 0,
+        ids: Sequence[int] | None = None,
     ) -> list[int]:
         """Register `n_adapters` random adapters directly on the device.
 
@@ -342,9 +343,9 @@ class AdapterPool:
         """
         g = torch.Generator(device=self.device)
         g.manual_seed(seed)
+        wanted = list(ids) if ids is not None else [first_id + i for i in range(n_adapters)]
         ids = []
-        for i in range(n_adapters):
-            aid = first_id + i
+        for aid in wanted:
             if aid in self._slots:
                 raise StateError(f"adapter {aid} is already registered")
             free = self._free_lora if kind is AdapterKind.LORA else self._free_reft

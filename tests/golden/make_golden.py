@@ -285,7 +285,22 @@ def gen_init_and_io():
     np.savez_compressed(OUT / "init_io.npz", **out)
 
 
+def gen_workload():
+    """Punica request streams (workload.py:110-156) for every mix."""
+    from prefillsim import workload as W
+
+    out = {}
+    for mix in W.AdapterMix:
+        cfg = W.WorkloadConfig(1000, 512, mix, seed=3, l_max=2048)
+        p = W.sample_prompt_lens(cfg)
+        out[f"{mix.value}_prompt"] = p
+        out[f"{mix.value}_total"] = W.sample_total_lens(cfg, p)
+        out[f"{mix.value}_adapters"] = np.asarray(W.assign_adapters(cfg), dtype=np.int64)
+    np.savez_compressed(OUT / "workload.npz", **out)
+
+
 def main():
+    gen_workload()
     nb = gen_masks()
     nd = gen_deltas()
     nm = gen_masked()
