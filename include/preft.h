@@ -123,7 +123,8 @@ typedef struct preft_meta {
     int32_t tile_cap;    /* >= E_cap + T_cap / tile_tokens + 1 */
     int32_t tile_tokens; /* tokens per work tile (>= 1) */
     int32_t slot_split;  /* first ReFT slot; slots below it are LoRA slots */
-    int32_t reserved;
+    int32_t rows_hint;   /* host's expected token count (0 = unknown): picks the
+                            K2 team size at launch; never affects results */
 } preft_meta_t;
 
 #define PREFT_MAX_ENTRIES 4096
@@ -209,6 +210,13 @@ int preft_plan_num_ops(const preft_plan_t* plan);
 int preft_plan_set_timing(preft_plan_t* plan, int32_t tag, int32_t reserve_pairs);
 int preft_plan_run(preft_plan_t* plan, int32_t run_meta, void* stream);
 int preft_plan_collect_timing(preft_plan_t* plan, double* total_ms, int32_t* count);
+
+/* K2 kernel variant: -1 automatic (default: team kernel with the team size
+ * chosen from the row widths), 0 warp-per-row kernel only, 1/2/4/8 team
+ * kernel with that many warps per row where eligible (aligned rows,
+ * r_max <= 4, bf16/f32).  For A/B measurement and for testing every code
+ * path; results agree to the stated tolerance.  Env: PREFT_LORA_VARIANT. */
+int preft_set_lora_variant(int32_t variant);
 
 /* library / device introspection */
 int preft_abi_version(void);

@@ -57,7 +57,7 @@ class PreftMeta(ctypes.Structure):
         ("tile_cap", ctypes.c_int32),
         ("tile_tokens", ctypes.c_int32),
         ("slot_split", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("rows_hint", ctypes.c_int32),
     ]
 
 
@@ -163,6 +163,7 @@ SIGNATURES = {
         ctypes.c_int,
         [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)],
     ),
+    "preft_set_lora_variant": (ctypes.c_int, [ctypes.c_int32]),
     "preft_abi_version": (ctypes.c_int, []),
     "preft_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "preft_last_cuda_error": (ctypes.c_char_p, []),

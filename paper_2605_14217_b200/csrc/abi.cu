@@ -60,6 +60,7 @@ int grid_for(const void* fn, int threads, int num_sms) {
     return num_sms * per_sm;
 }
 
+void set_lora_variant(int v);
 int plan_num_sms() { return current_num_sms(); }
 int plan_record_cuda(cudaError_t e) { return record_cuda(e); }
 
@@ -118,6 +119,13 @@ const char* preft_status_string(int status) {
 const char* preft_last_cuda_error(void) { return g_last_cuda_error; }
 
 int preft_num_sms(void) { return current_num_sms(); }
+
+int preft_set_lora_variant(int32_t variant) {
+    if (variant != -1 && variant != 0 && variant != 1 && variant != 2 && variant != 4 && variant != 8)
+        return PREFT_ERR_DOMAIN;
+    set_lora_variant(variant);
+    return PREFT_OK;
+}
 
 size_t preft_meta_entries_words(int32_t E_cap) { return 2 + static_cast<size_t>(E_cap) * 3 + 1; }
 

@@ -154,6 +154,8 @@ __global__ void __launch_bounds__(256) lora_kernel(const LoraArgs a) {
     }
 }
 
+#include "lora_team.cuh"
+
 // ------------------------------------------------------------------ dispatch
 
 using LoraFn = void (*)(LoraArgs);
@@ -187,6 +189,19 @@ LoraFn pick_lora(bool vec, int nsites, int r) {
 }
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// -1 = automatic, 0 = warp-per-row only, 1 = CTA-per-row where eligible
+static int g_lora_variant = -2;
+int lora_variant() {
+    if (g_lora_variant == -2) {
+        const char* env = getenv("PREFT_LORA_VARIANT");
+        g_lora_variant = -1;
+        if (env && env[0] == 'w') g_lora_variant = 0;
+        if (env && (env[0] == '1' || env[0] == '2' || env[0] == '4' || env[0] == '8')) g_lora_variant = env[0] - '0';
+    }
+    return g_lora_variant;
+}
+void set_lora_variant(int v) { g_lora_variant = v; }
 
 int grid_for(const void* fn, int threads, int num_sms);
 
@@ -225,9 +240,23 @@ int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, co
     }
     args.tokens = reinterpret_cast<const int2*>(meta->tokens);
     args.counters = meta->counters;
-    LoraFn fn = dtype == PREFT_DTYPE_BF16  ? pick_lora<__nv_bfloat16>(vec, nsites, r)
-                : dtype == PREFT_DTYPE_F32 ? pick_lora<float>(vec, nsites, r)
-                                           : pick_lora<double>(vec, nsites, r);
+    // variant: team kernel (lora_team.cuh) for aligned rank<=4 bf16/f32 rows,
+    // team size from the row widths unless forced (preft_set_lora_variant:
+    // 0 = warp kernel above, 1/2/4/8 = team warps; PREFT_LORA_VARIANT env)
+    const int variant = lora_variant();
+    LoraFn fn = nullptr;
+    if (variant != 0 && vec && r <= 4 && dtype != PREFT_DTYPE_F64) {
+        int nvt = 0;
+        for (int s = 0; s < nsites; ++s) nvt += sites[s].n / W;
+        (void)nvt;
+        const int team = variant > 0 ? variant : auto_team_warps(meta->rows_hint, num_sms);
+        fn = reinterpret_cast<LoraFn>(dtype == PREFT_DTYPE_BF16 ? pick_lora_team<__nv_bfloat16>(nsites, r, team)
+                                                                : pick_lora_team<float>(nsites, r, team));
+    }
+    if (!fn)
+        fn = dtype == PREFT_DTYPE_BF16  ? pick_lora<__nv_bfloat16>(vec, nsites, r)
+             : dtype == PREFT_DTYPE_F32 ? pick_lora<float>(vec, nsites, r)
+                                        : pick_lora<double>(vec, nsites, r);
     if (!fn) return PREFT_ERR_RANK;
     const int grid = grid_for(reinterpret_cast<const void*>(fn), 256, num_sms);
     fn<<<grid, 256, 0, stream>>>(args);

@@ -78,6 +78,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
     extern __shared__ __align__(16) unsigned char smem_raw[];
     __shared__ int s_warp[32];
     __shared__ int s_total;
+    __shared__ int s_split;
     __shared__ int s_err;
 
     const int tid = threadIdx.x;
@@ -167,14 +168,16 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
     const int n_tok = block_scan_array(A, nsel, s_warp, &s_total);
     const int nseg = block_scan_array(B, nsel, s_warp, &s_total);
 
-    if (tid == 0) s_total = n_tok;  // tokens below the LoRA/ReFT slot split
+    // tokens below the LoRA/ReFT slot split (own shared slot: s_total may
+    // still be being read by threads returning from the last scan)
+    if (tid == 0) s_split = n_tok;
     __syncthreads();
     for (int i = tid; i < nsel; i += blockDim.x) {
         const int sl = static_cast<int>(keys[i] >> 32);
-        if (sl >= m.slot_split && (i == 0 || static_cast<int>(keys[i - 1] >> 32) < m.slot_split)) s_total = A[i];
+        if (sl >= m.slot_split && (i == 0 || static_cast<int>(keys[i - 1] >> 32) < m.slot_split)) s_split = A[i];
     }
     __syncthreads();
-    const int n_split = s_total;
+    const int n_split = s_split;
     for (int i = tid; i < nsel; i += blockDim.x) {
         const unsigned long long k = keys[i];
         const int e = static_cast<int>(k & 0xffffffffu);

@@ -141,6 +141,7 @@ class BatchMeta:
             ev = torch.cuda.Event()
             ev.record(s)
             self._staged = ev
+        self.c.rows_hint = T  # launch-shape hint for K2 (team size); results never depend on it
         _lib.check(_lib.load().preft_meta_build(ctypes.byref(self.c), ctypes.c_void_p(s.cuda_stream)), "meta_build")
         self.E, self.T = E, T
         return self

@@ -109,6 +109,46 @@ def test_random_batches_groups_ranks(cuda_device, mode, rank, group):
         helpers.check_close(out, yi, ref, mode, f"{s} r={rank}")
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2, 4, 8, -1])
+@pytest.mark.parametrize("mode", ["f32", "bf16"])
+@pytest.mark.parametrize("rank", [1, 2, 4])
+def test_team_and_warp_variants(cuda_device, variant, mode, rank):
+    """Every K2 variant (warp-per-row kernel; team kernel with 1/2/4/8 warps
+    per row; automatic) against the oracle on aligned widths."""
+    from paper_2605_14217_b200 import _lib
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_group_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    sites = {"Wq": (2048, 2048), "Wk": (512, 2048), "Wv": (512, 2048), "Wgate": (6144, 2048), "Wup": (6144, 2048),
+             "Wdown": (2048, 6144)}
+    rng = np.random.default_rng(rank * 3 + variant)
+    dtype = MODES[mode]
+    pool = AdapterPool(1, 2048, lora_sites=sites, lora_capacity=6, lora_rank=rank, dtype=dtype, device=cuda_device)
+    for aid in range(6):
+        pool.register(U.random_lora_adapter(rng, aid, 1, sites, rank))
+    meta = BatchMeta(128, 4096, device=cuda_device)
+    qsl, ids, flags = U.random_entries(rng, 40, list(range(6)), max_len=24)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    T = int(qsl[-1])
+    lib = _lib.load()
+    try:
+        assert lib.preft_set_lora_variant(variant) == 0
+        for group in (("Wq", "Wk", "Wv"), ("Wgate", "Wup"), ("Wdown",)):
+            x = U.rand_act(rng, T, sites[group[0]][1], dtype, cuda_device)
+            ys = [U.rand_act(rng, T, sites[s][0], dtype, cuda_device) for s in group]
+            y_in = [U.to_np(y) for y in ys]
+            apply_lora_group_(ys, x, meta, pool, 0, group)
+            mask = U.oracle_mask(qsl, slots, flags)
+            for s, y, yi in zip(group, ys, y_in):
+                out = U.to_np(y)
+                assert np.array_equal(out[~mask], yi[~mask])
+                ref = U.lora_oracle(yi, U.to_np(x), qsl, slots, flags, pool, 0, s)
+                helpers.check_close(out, yi, ref, mode, f"variant {variant} {s} r={rank}")
+    finally:
+        lib.preft_set_lora_variant(-1)
+
+
 @pytest.mark.parametrize("mode", ["f32", "bf16"])
 def test_odd_widths_use_scalar_path(cuda_device, mode):
     from paper_2605_14217_b200.meta import BatchMeta
