@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-punica-step", action="store_true")
+    p.add_argument("--no-secondary", action="store_true", help="skip the config-1/3/5 secondary lines")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU baseline sample length")
     p.add_argument("--ref-requests", type=int, default=4, help="reference arm: requests per worker per step")
     return p.parse_args()
@@ -253,7 +254,7 @@ def build_step(args, rank, world, device, n_prefill, n_decode, seed=SEED):
     pool.fill_synthetic_(0, AdapterKind.LORA, RANK, seed=seed + 17 * rank, sigma=0.01, ids=owned)
     slots = pool.entry_arrays(qsl, ids, flags)
     E, T = len(ids), int(qsl[-1])
-    meta = BatchMeta(E, T, tile_tokens=16, device=device)
+    meta = BatchMeta(E, T, tile_tokens=128, device=device)
     meta.set_slot_split(pool.slot_split)
     meta.build_arrays(qsl, slots, flags)  # entries now resident in HBM
     dims = shape.site_dims()
@@ -408,6 +409,125 @@ def punica_step(args, rank, world, device):
     return out
 
 
+def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, steps: int = 5) -> dict:
+    """Secondary line: a ReFT^P residual site x 32 layers (8B shapes) over one
+    batch of long prompts, one fused launch per layer (BASELINE configs 3/5)."""
+    import torch
+
+    from paper_2605_14217_b200 import AdapterKind, shapes
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.plan import StepPlan
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    d = shapes.LLAMA_8B.d_model
+    kind = AdapterKind(kind_name)
+    pool = AdapterPool(N_LAYERS, d, reft_capacity=N_ADAPTERS, reft_rank=rank, dtype=torch.bfloat16, device=device)
+    pool.fill_synthetic_(N_ADAPTERS, kind, rank, seed=5)
+    n_dec = 64
+    all_lens = np.concatenate([np.ones(n_dec, dtype=np.int64), np.asarray(lens, dtype=np.int64)])
+    qsl = np.concatenate([[0], np.cumsum(all_lens)]).astype(np.int32)
+    flags = np.array([1] * n_dec + [0] * len(lens), dtype=np.int32)
+    eids = [int(i) % N_ADAPTERS for i in range(n_dec)] + [int(a) for a in ids]
+    slots = pool.entry_arrays(qsl, eids, flags)
+    T = int(qsl[-1])
+    meta = BatchMeta(len(eids), T, tile_tokens=128, device=device)
+    meta.set_slot_split(pool.slot_split)
+    meta.build_arrays(qsl, slots, flags)
+    h = torch.randn(T, d, device=device, dtype=torch.float32).to(torch.bfloat16)
+    plan = StepPlan(meta, pool, max_tokens=T)
+    for layer in range(N_LAYERS):
+        plan.add_reft(h, layer, tag=1)
+    s = torch.cuda.current_stream(device)
+    for _ in range(2):
+        plan.run(s)
+    plan.set_timing(1, steps * N_LAYERS)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        plan.run(s)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    k_ms, k_n = plan.collect_timing()
+    sel = int(np.sum(lens))
+    distinct = len(set(int(a) for a in ids))
+    per_launch = sel * 2 * d * 2 + distinct * 2 * (2 * rank * d) + distinct * 4 * rank
+    peak, _ = measured_peak_gbs()
+    frac = per_launch / (k_ms / k_n / 1e3) / 1e9 / peak
+    out = {"workload": label, "prefill_tokens": sel, "ms_per_step": round(ms, 3),
+           "value": round(sel / (ms / 1e3), 1), "unit": UNIT, "kernel_frac_of_hbm_peak": round(frac, 4),
+           "avg_launch_us": round(k_ms / k_n * 1e3, 2)}
+    del pool, meta, plan, h
+    torch.cuda.empty_cache()
+    return out
+
+
+def lora_reft_mix_config(args, device) -> dict:
+    """Config 1 on the GPU: one layer, d = 4096, 16 DiReFT^P r=8 + 16 LoRA^P r=1
+    (one 4096->4096 site), 32 prefill x 128 + 32 decode tokens."""
+    import torch
+
+    from paper_2605_14217_b200 import AdapterKind
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_, apply_reft_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    d = 4096
+    pool = AdapterPool(1, d, lora_sites={"Wq": (d, d)}, lora_capacity=16, lora_rank=1, reft_capacity=16,
+                       reft_rank=8, dtype=torch.bfloat16, device=device)
+    lora_ids = pool.fill_synthetic_(16, AdapterKind.LORA, 1, seed=1, ids=list(range(16, 32)))
+    reft_ids = pool.fill_synthetic_(16, AdapterKind.DIREFT, 8, seed=2, ids=list(range(16)))
+    lens = [1] * 32 + [128] * 32
+    qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    flags = np.array([1] * 32 + [0] * 32, dtype=np.int32)
+    eids = [i % 32 for i in range(32)] + list(range(32))
+    slots = pool.entry_arrays(qsl, eids, flags)
+    meta = BatchMeta(64, int(qsl[-1]), device=device)
+    meta.set_slot_split(pool.slot_split)
+    meta.build_arrays(qsl, slots, flags)
+    T = int(qsl[-1])
+    x = torch.randn(T, d, device=device).to(torch.bfloat16)
+    y = torch.randn(T, d, device=device).to(torch.bfloat16)
+    h = torch.randn(T, d, device=device).to(torch.bfloat16)
+    s = torch.cuda.current_stream(device)
+    for _ in range(3):
+        apply_lora_(y, x, meta, pool, 0, "Wq")
+        apply_reft_(h, meta, pool, 0)
+    torch.cuda.synchronize()
+    n = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(n):
+        meta.launch(s)
+        apply_lora_(y, x, meta, pool, 0, "Wq")
+        apply_reft_(h, meta, pool, 0)
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / n
+    del pool, meta
+    torch.cuda.empty_cache()
+    return {"workload": "cfg1: 1 layer d=4096, 16 DiReFT^P r8 + 16 LoRA^P r1, 32x128 prefill + 32 decode",
+            "prefill_tokens": 4096, "ms_per_step": round(ms, 4),
+            "value": round(4096 / (ms / 1e3), 1), "unit": "tokens/s per (layer, site pair)"}
+
+
+def secondary_configs(args, device) -> list:
+    from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig, assign_adapters
+
+    out = [lora_reft_mix_config(args, device)]
+    rng = np.random.default_rng(3)
+    ids3 = rng.integers(0, N_ADAPTERS, size=32)
+    out.append(reft_config(args, device, "direft", 16, [2048] * 32, ids3,
+                           "cfg3 slice (1 GPU): 8B shapes, DiReFT^P r16 x 32 layers, 512 adapters, 32 x 2048-token "
+                           "prompts + 64 decode"))
+    ids5 = assign_adapters(WorkloadConfig(8, N_ADAPTERS, AdapterMix.SKEWED, seed=5))
+    lens5 = rng.integers(8192, 16385, size=8)
+    out.append(reft_config(args, device, "loreft", 32, lens5, ids5,
+                           "cfg5 slice (1 GPU): Zipf over 512 adapters, 8 prompts U[8k,16k], LoReFT^P r32 x 32 layers"))
+    return out
+
+
 def cpu_baseline(ctx, seconds: float) -> dict:
     """The reference CPU path (float64 numpy oracle) on one host core, on a
     bounded sample of the same workload: the first 8 prefill requests (plus
@@ -460,6 +580,11 @@ def run_ours(args):
     punica = None
     if not args.no_punica_step and world == 1:
         punica = punica_step(args, rank, world, device)
+    others = None
+    if not args.no_secondary and world == 1:
+        del ctx["plan"], ctx["acts"]
+        torch.cuda.empty_cache()
+        others = secondary_configs(args, device)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(ctx, args.cpu_seconds)
@@ -514,6 +639,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "punica_step": punica,
+            "other_configs": others,
         }
         print(json.dumps(line))
     if world > 1:

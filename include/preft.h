@@ -173,10 +173,18 @@ int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32
  * A = W - R, B = R.  Pool layout for this layer: A [S][r_max][d],
  * B [S][r_max][d], bias [S][r_max], scale [S] (bias/scale in the accumulator
  * type: f32 for F32/BF16, f64 for F64).  r_max in {1,2,4,8,16,32,64}.
+ * Bt [S][d][r_max] (B transposed, K-major for the tensor-core expand) may be
+ * NULL; when given, bf16 with r_max in {16, 32}, d in {1024, 2048, 4096} and
+ * meta->tile_tokens <= 128 runs the tcgen05 kernel (a d/512-CTA cluster per
+ * 128-token tile, TMEM accumulators); everything else runs the SIMT kernel.
  */
 int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t ldh, int32_t d,
-                     const void* A, const void* B, const void* bias, const void* scale,
-                     int32_t r_max, int32_t dtype, void* stream);
+                     const void* A, const void* B, const void* Bt, const void* bias,
+                     const void* scale, int32_t r_max, int32_t dtype, void* stream);
+
+/* K3 kernel variant: -1 automatic (default), 0 SIMT only, 1 tensor cores
+ * only (PREFT_ERR_SHAPE when ineligible).  Env: PREFT_REFT_VARIANT=simt|tc. */
+int preft_set_reft_variant(int32_t variant);
 
 /*
  * K4: dst[i*dst_ld + j] = convert(src[i*src_stride_row + j*src_stride_col])
@@ -204,8 +212,8 @@ int preft_plan_add_lora(preft_plan_t* plan, const void* x, int64_t ldx, int32_t 
                         const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
                         int32_t dtype, int32_t tag);
 int preft_plan_add_reft(preft_plan_t* plan, void* h, int64_t ldh, int32_t d, const void* A,
-                        const void* B, const void* bias, const void* scale, int32_t r_max,
-                        int32_t dtype, int32_t tag);
+                        const void* B, const void* Bt, const void* bias, const void* scale,
+                        int32_t r_max, int32_t dtype, int32_t tag);
 int preft_plan_num_ops(const preft_plan_t* plan);
 int preft_plan_set_timing(preft_plan_t* plan, int32_t tag, int32_t reserve_pairs);
 int preft_plan_run(preft_plan_t* plan, int32_t run_meta, void* stream);
@@ -217,6 +225,11 @@ int preft_plan_collect_timing(preft_plan_t* plan, double* total_ms, int32_t* cou
  * r_max <= 4, bf16/f32).  For A/B measurement and for testing every code
  * path; results agree to the stated tolerance.  Env: PREFT_LORA_VARIANT. */
 int preft_set_lora_variant(int32_t variant);
+
+/* Diagnostic: D[128 x N] (f32) = A[128 x K] . B[N x K]^T (bf16, row-major,
+ * device) through the tcgen05/TMEM path the tensor-core kernels use
+ * (K % 16 == 0, N % 16 == 0, 16 <= N <= 256).  Pins the UMMA descriptors. */
+int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t N, void* stream);
 
 /* library / device introspection */
 int preft_abi_version(void);

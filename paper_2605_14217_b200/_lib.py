@@ -103,11 +103,13 @@ SIGNATURES = {
             ctypes.c_void_p,
             ctypes.c_void_p,
             ctypes.c_void_p,
+            ctypes.c_void_p,
             ctypes.c_int32,
             ctypes.c_int32,
             ctypes.c_void_p,
         ],
     ),
+    "preft_set_reft_variant": (ctypes.c_int, [ctypes.c_int32]),
     "preft_convert_2d": (
         ctypes.c_int,
         [
@@ -151,6 +153,7 @@ SIGNATURES = {
             ctypes.c_void_p,
             ctypes.c_void_p,
             ctypes.c_void_p,
+            ctypes.c_void_p,
             ctypes.c_int32,
             ctypes.c_int32,
             ctypes.c_int32,
@@ -164,6 +167,10 @@ SIGNATURES = {
         [ctypes.c_void_p, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_int32)],
     ),
     "preft_set_lora_variant": (ctypes.c_int, [ctypes.c_int32]),
+    "preft_tc_selftest": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p],
+    ),
     "preft_abi_version": (ctypes.c_int, []),
     "preft_status_string": (ctypes.c_char_p, [ctypes.c_int]),
     "preft_last_cuda_error": (ctypes.c_char_p, []),

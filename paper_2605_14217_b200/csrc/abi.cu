@@ -12,7 +12,9 @@ int meta_build(const preft_meta_t* m, cudaStream_t stream, int num_sms);
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
                int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
 int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
-               const void* bias, const void* scale, int r, int dtype, cudaStream_t stream, int num_sms);
+               const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
+               int num_sms);
+void set_reft_variant(int v);
 
 static thread_local char g_last_cuda_error[256] = "";
 
@@ -61,6 +63,7 @@ int grid_for(const void* fn, int threads, int num_sms) {
 }
 
 void set_lora_variant(int v);
+int tc_selftest(const void* A, const void* B, float* D, int K, int N, cudaStream_t s);
 int plan_num_sms() { return current_num_sms(); }
 int plan_record_cuda(cudaError_t e) { return record_cuda(e); }
 
@@ -120,6 +123,10 @@ const char* preft_last_cuda_error(void) { return g_last_cuda_error; }
 
 int preft_num_sms(void) { return current_num_sms(); }
 
+int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t N, void* stream) {
+    return finish(tc_selftest(A, B, D, K, N, static_cast<cudaStream_t>(stream)));
+}
+
 int preft_set_lora_variant(int32_t variant) {
     if (variant != -1 && variant != 0 && variant != 1 && variant != 2 && variant != 4 && variant != 8)
         return PREFT_ERR_DOMAIN;
@@ -148,9 +155,15 @@ int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32
 }
 
 int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t ldh, int32_t d, const void* A, const void* B,
-                     const void* bias, const void* scale, int32_t r_max, int32_t dtype, void* stream) {
-    return finish(reft_apply(meta, h, ldh, d, A, B, bias, scale, r_max, dtype, static_cast<cudaStream_t>(stream),
+                     const void* Bt, const void* bias, const void* scale, int32_t r_max, int32_t dtype, void* stream) {
+    return finish(reft_apply(meta, h, ldh, d, A, B, Bt, bias, scale, r_max, dtype, static_cast<cudaStream_t>(stream),
                              current_num_sms()));
+}
+
+int preft_set_reft_variant(int32_t variant) {
+    if (variant < -1 || variant > 1) return PREFT_ERR_DOMAIN;
+    set_reft_variant(variant);
+    return PREFT_OK;
 }
 
 int preft_convert_2d(void* dst, int32_t dst_dtype, int64_t dst_ld, const double* src, int64_t src_stride_row,

@@ -14,7 +14,8 @@ int meta_build(const preft_meta_t* m, cudaStream_t stream, int num_sms);
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
                int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
 int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
-               const void* bias, const void* scale, int r, int dtype, cudaStream_t stream, int num_sms);
+               const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
+               int num_sms);
 int plan_num_sms();
 int plan_record_cuda(cudaError_t e);
 }  // namespace preft
@@ -30,7 +31,7 @@ struct PlanOp {
     int r;
     int dtype;
     preft_lora_site_t sites[3];
-    const void *A, *B, *bias, *scale;
+    const void *A, *B, *Bt, *bias, *scale;
 };
 
 struct preft_plan {
@@ -45,7 +46,7 @@ using namespace preft;
 
 static int plan_launch(preft_plan* p, const PlanOp& op, cudaStream_t s, int sms) {
     if (op.kind == 0) return lora_apply(&p->meta, op.x, op.ld, op.width, op.sites, op.nsites, op.r, op.dtype, s, sms);
-    return reft_apply(&p->meta, op.h, op.ld, op.width, op.A, op.B, op.bias, op.scale, op.r, op.dtype, s, sms);
+    return reft_apply(&p->meta, op.h, op.ld, op.width, op.A, op.B, op.Bt, op.bias, op.scale, op.r, op.dtype, s, sms);
 }
 
 extern "C" {
@@ -87,7 +88,8 @@ int preft_plan_add_lora(preft_plan* p, const void* x, int64_t ldx, int32_t m, co
 }
 
 int preft_plan_add_reft(preft_plan* p, void* h, int64_t ldh, int32_t d, const void* A, const void* B,
-                        const void* bias, const void* scale, int32_t r_max, int32_t dtype, int32_t tag) {
+                        const void* Bt, const void* bias, const void* scale, int32_t r_max, int32_t dtype,
+                        int32_t tag) {
     if (!p) return PREFT_ERR_SHAPE;
     PlanOp op{};
     op.kind = 1;
@@ -97,6 +99,7 @@ int preft_plan_add_reft(preft_plan* p, void* h, int64_t ldh, int32_t d, const vo
     op.width = d;
     op.A = A;
     op.B = B;
+    op.Bt = Bt;
     op.bias = bias;
     op.scale = scale;
     op.r = r_max;

@@ -181,11 +181,33 @@ static bool aligned16r(const void* p) { return (reinterpret_cast<uintptr_t>(p) &
 
 int grid_for(const void* fn, int threads, int num_sms);
 
+int reft_tc_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* Bt,
+                  const void* bias, const void* scale, int r, cudaStream_t stream);
+
+// -1 automatic (tensor cores when eligible), 0 SIMT only, 1 tensor cores only
+static int g_reft_variant = -2;
+int reft_variant() {
+    if (g_reft_variant == -2) {
+        const char* env = getenv("PREFT_REFT_VARIANT");
+        g_reft_variant = (env && env[0] == 's') ? 0 : (env && env[0] == 't') ? 1 : -1;
+    }
+    return g_reft_variant;
+}
+void set_reft_variant(int v) { g_reft_variant = v; }
+
 int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
-               const void* bias, const void* scale, int r, int dtype, cudaStream_t stream, int num_sms) {
+               const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
+               int num_sms) {
     if (!meta || !h || !A || !B || !bias || !scale || d < 1 || ldh < d) return PREFT_ERR_SHAPE;
     if (r < 1 || r > 64 || (r & (r - 1))) return PREFT_ERR_RANK;
     if (dtype != PREFT_DTYPE_F32 && dtype != PREFT_DTYPE_BF16 && dtype != PREFT_DTYPE_F64) return PREFT_ERR_DOMAIN;
+    const int variant = reft_variant();
+    if (variant != 0 && Bt && dtype == PREFT_DTYPE_BF16) {
+        const int rc = reft_tc_apply(meta, h, ldh, d, A, Bt, bias, scale, r, stream);
+        if (rc != PREFT_ERR_SHAPE || variant == 1) return rc;  // launched, failed, or TC forced
+    } else if (variant == 1) {
+        return PREFT_ERR_SHAPE;
+    }
     const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;
     const bool vec = (d % W == 0) && (ldh % W == 0) && aligned16r(h) && aligned16r(A) && aligned16r(B);
     const int dv = vec ? d / W : d;

@@ -56,7 +56,7 @@ def pack_entries(batch: ForwardBatch, slot_of: Mapping[int, int]) -> tuple[np.nd
 class BatchMeta:
     """Fixed-capacity device workspace for one in-flight step."""
 
-    def __init__(self, max_entries: int, max_tokens: int, tile_tokens: int = 16, device=None):
+    def __init__(self, max_entries: int, max_tokens: int, tile_tokens: int = 128, device=None):
         if not 1 <= max_entries <= _lib.MAX_ENTRIES:
             raise InfeasibleBatchError(f"max_entries must be in [1, {_lib.MAX_ENTRIES}], got {max_entries}")
         if max_tokens < 1 or tile_tokens < 1:

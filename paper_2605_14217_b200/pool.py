@@ -115,6 +115,8 @@ class AdapterPool:
         L, dev = self.n_layers, self.device
         z = dict(dtype=dtype, device=dev)
         za = dict(dtype=self.acc, device=dev)
+        self.reft_Bt: torch.Tensor | None = None
+        self.reft_tc = False
         self.lora_A: dict[str, torch.Tensor] = {}
         self.lora_Bt: dict[str, torch.Tensor] = {}
         self.lora_scale: dict[str, torch.Tensor] = {}
@@ -127,6 +129,9 @@ class AdapterPool:
             S, R, d = self.reft_capacity, self.reft_rank, self.d_model
             self.reft_A = torch.zeros(L, S, R, d, **z)
             self.reft_B = torch.zeros(L, S, R, d, **z)
+            # K-major copy of B for the tcgen05 expand (csrc/reft_tc.cu): bf16, r 16/32, d = 512 x {2,4,8}
+            self.reft_tc = dtype == torch.bfloat16 and R in (16, 32) and d % 512 == 0 and d // 512 in (2, 4, 8)
+            self.reft_Bt = torch.zeros(L, S, d, R, **z) if self.reft_tc else None
             self.reft_bias = torch.zeros(L, S, R, **za)
             self.reft_scale = torch.zeros(L, S, **za)
         self._slots: dict[int, SlotInfo] = {}
@@ -155,6 +160,8 @@ class AdapterPool:
         tensors: list[torch.Tensor] = [*self.lora_A.values(), *self.lora_Bt.values(), *self.lora_scale.values()]
         if self.reft_capacity:
             tensors += [self.reft_A, self.reft_B, self.reft_bias, self.reft_scale]
+            if self.reft_Bt is not None:
+                tensors.append(self.reft_Bt)
         return sum(t.numel() * t.element_size() for t in tensors)
 
     def _validate(self, adapter: ModelAdapter) -> None:
@@ -291,12 +298,18 @@ class AdapterPool:
         else:
             R, d = self.reft_rank, self.d_model
             j = slot - self.slot_split
+            if self.reft_Bt is not None:
+                self.reft_Bt[:, j].zero_()  # columns >= rank stay zero
             sc = np.zeros(self.n_layers)
             for layer, p in enumerate(adapter.reft_sites):
                 shrink, expand, bias = p.device_operands()
                 r = p.rank
                 plan.append((self.reft_A[layer, j], self.dtype_code, add(shrink), d, 1, r, R, d))
-                plan.append((self.reft_B[layer, j], self.dtype_code, add(expand), d, 1, r, R, d))
+                o_exp = add(expand)
+                plan.append((self.reft_B[layer, j], self.dtype_code, o_exp, d, 1, r, R, d))
+                if self.reft_Bt is not None:
+                    # Bt[n][k] = B[k][n]: rows n < d, columns k < r of an (d, R) slot view
+                    plan.append((self.reft_Bt[layer, j], self.dtype_code, o_exp, 1, d, d, d, r))
                 plan.append((self.reft_bias[layer, j].unsqueeze(1), acc_code, add(bias), 1, 1, r, R, 1))
                 sc[layer] = p.prefactor
             plan.append((self.reft_scale[:, j].unsqueeze(1), acc_code, add(sc), 1, 1, self.n_layers, self.n_layers, 1))
@@ -316,6 +329,8 @@ class AdapterPool:
             j = info.slot - self.slot_split
             self.reft_A[:, j].zero_()
             self.reft_B[:, j].zero_()
+            if self.reft_Bt is not None:
+                self.reft_Bt[:, j].zero_()
             self.reft_bias[:, j].zero_()
             self.reft_scale[:, j].zero_()
 
@@ -376,7 +391,10 @@ class AdapterPool:
                 b = torch.randn(len(ids), rank, generator=g, device=self.device) * 0.1
                 pad = self.reft_rank - rank
                 self.reft_A[layer].index_copy_(0, js, torch.nn.functional.pad(A, (0, 0, 0, pad)).to(self.dtype))
-                self.reft_B[layer].index_copy_(0, js, torch.nn.functional.pad(B, (0, 0, 0, pad)).to(self.dtype))
+                Bp = torch.nn.functional.pad(B, (0, 0, 0, pad)).to(self.dtype)
+                self.reft_B[layer].index_copy_(0, js, Bp)
+                if self.reft_Bt is not None:
+                    self.reft_Bt[layer].index_copy_(0, js, Bp.transpose(1, 2).contiguous())
                 self.reft_bias[layer].index_copy_(0, js, torch.nn.functional.pad(b, (0, pad)).to(self.acc))
             self.reft_scale.index_fill_(1, js, 1.0 / np.sqrt(rank))
         return ids

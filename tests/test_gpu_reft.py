@@ -66,6 +66,63 @@ def test_zero_delta_adapters_leave_stream_bit_identical(cuda_device, kind):
     assert torch.equal(h, h0)
 
 
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("rank", [16, 32])
+@pytest.mark.parametrize("d", [1024, 2048, 4096])
+def test_tensor_core_and_simt_variants(cuda_device, variant, rank, d):
+    """The tcgen05 cluster kernel (variant 1) and the SIMT kernel (variant 0)
+    on the same mixed batch: short and multi-tile segments, decode and
+    adapter-less entries, and LoRA-class tokens interleaved in the sorted list
+    (the ReFT kernel must skip their tiles)."""
+    from paper_2605_14217_b200 import _lib
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_, apply_reft_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(d + rank + variant)
+    sites = {"Wq": (d, d)}
+    pool = AdapterPool(1, d, lora_sites=sites, lora_capacity=3, lora_rank=1, reft_capacity=6, reft_rank=rank,
+                       dtype=torch.bfloat16, device=cuda_device)
+    assert pool.reft_tc
+    for aid in range(3):
+        pool.register(U.random_lora_adapter(rng, 100 + aid, 1, sites, 1))
+    for aid in range(6):
+        kind = AdapterKind.DIREFT if aid % 2 else AdapterKind.LOREFT
+        pool.register(U.random_reft_adapter(rng, aid, 1, d, rank if aid < 4 else rank // 2, kind))
+    lens = [1] * 10 + list(rng.integers(1, 40, size=20)) + [300, 129, 128, 700]
+    qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    ids, flags = [], []
+    for i, n in enumerate(lens):
+        pick = rng.integers(0, 10)
+        ids.append(None if pick == 9 else (100 + pick % 3 if pick >= 6 else int(pick % 6)))
+        flags.append(_lib.ENTRY_DECODE if n == 1 and i < 10 else 0)
+    flags = np.asarray(flags, dtype=np.int32)
+    meta = BatchMeta(64, int(qsl[-1]), device=cuda_device)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    T = int(qsl[-1])
+    h = U.rand_act(rng, T, d, torch.bfloat16, cuda_device)
+    x = U.rand_act(rng, T, d, torch.bfloat16, cuda_device)
+    y = U.rand_act(rng, T, d, torch.bfloat16, cuda_device)
+    h_in, y_in = U.to_np(h), U.to_np(y)
+    lib = _lib.load()
+    try:
+        assert lib.preft_set_reft_variant(variant) == 0
+        apply_lora_(y, x, meta, pool, 0, "Wq")
+        apply_reft_(h, meta, pool, 0)
+        torch.cuda.synchronize()
+    finally:
+        lib.preft_set_reft_variant(-1)
+    mask = U.oracle_mask(qsl, slots, flags)
+    out = U.to_np(h)
+    assert np.array_equal(out[~mask], h_in[~mask])
+    ref = U.reft_oracle(h_in, qsl, slots, flags, pool, 0)
+    helpers.check_close(out, h_in, ref, "bf16", f"reft variant {variant} d={d} r={rank}")
+    lora_rows = np.isin(slots, [pool.info(100 + a).slot for a in range(3)])
+    assert lora_rows.any()
+    yref = U.lora_oracle(y_in, U.to_np(x), qsl, slots, flags, pool, 0, "Wq")
+    helpers.check_close(U.to_np(y), y_in, yref, "bf16", "lora alongside reft")
+
+
 def test_long_segments_zipf(cuda_device):
     """Config-5-like shape at reduced size: few hot adapters, long prompts,
     LoReFT r=32, d=4096 bf16 (register-resident row path)."""

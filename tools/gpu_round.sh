@@ -28,8 +28,8 @@ EOF
 timeout 300 python tools/kbench.py > $O/${TAG}_kbench.json 2> $O/${TAG}_kbench.err
 timeout 300 python tools/kbench.py --requests 32 --decodes 32 > $O/${TAG}_kbench_small.json 2>> $O/${TAG}_kbench.err
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"lora|meta|reft" -c 390 --csv \
-  --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-punica-step \
+  --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-punica-step --no-secondary \
   > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:lora -s 2 -c 4 -o $O/${TAG}_prof \
-  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-punica-step > $O/${TAG}_ncu.log 2>&1
+  python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-punica-step --no-secondary > $O/${TAG}_ncu.log 2>&1
 ls $O | grep "^${TAG}_"
