@@ -168,7 +168,7 @@ int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32
                      int32_t dtype, void* stream);
 
 /*
- * K3: h[t,:] += s_a * ((h[t,:] . A_a^T + b_a) . B_a)   for every selected token
+ * K3 (h has `rows` allocated rows; TMA bounds): h[t,:] += s_a * ((h[t,:] . A_a^T + b_a) . B_a)   for every selected token
  * (adapters.py:292-295).  DiReFT: A, B as stored by the reference.  LoReFT:
  * A = W - R, B = R.  Pool layout for this layer: A [S][r_max][d],
  * B [S][r_max][d], bias [S][r_max], scale [S] (bias/scale in the accumulator
@@ -178,7 +178,7 @@ int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32
  * meta->tile_tokens <= 128 runs the tcgen05 kernel (a d/512-CTA cluster per
  * 128-token tile, TMEM accumulators); everything else runs the SIMT kernel.
  */
-int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t ldh, int32_t d,
+int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ldh, int32_t d,
                      const void* A, const void* B, const void* Bt, const void* bias,
                      const void* scale, int32_t r_max, int32_t dtype, void* stream);
 
@@ -211,7 +211,7 @@ int preft_plan_set_slot_split(preft_plan_t* plan, int32_t slot_split);
 int preft_plan_add_lora(preft_plan_t* plan, const void* x, int64_t ldx, int32_t m,
                         const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
                         int32_t dtype, int32_t tag);
-int preft_plan_add_reft(preft_plan_t* plan, void* h, int64_t ldh, int32_t d, const void* A,
+int preft_plan_add_reft(preft_plan_t* plan, void* h, int64_t rows, int64_t ldh, int32_t d, const void* A,
                         const void* B, const void* Bt, const void* bias, const void* scale,
                         int32_t r_max, int32_t dtype, int32_t tag);
 int preft_plan_num_ops(const preft_plan_t* plan);
@@ -228,8 +228,16 @@ int preft_set_lora_variant(int32_t variant);
 
 /* Diagnostic: D[128 x N] (f32) = A[128 x K] . B[N x K]^T (bf16, row-major,
  * device) through the tcgen05/TMEM path the tensor-core kernels use
- * (K % 16 == 0, N % 16 == 0, 16 <= N <= 256).  Pins the UMMA descriptors. */
-int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t N, void* stream);
+ * (K % 16 == 0, N % 16 == 0, 16 <= N <= 256).  mode 0: A staged by threads,
+ * no swizzle; 1: threads, 128 B swizzle; 2: TMA, 128 B swizzle (K % 64 == 0).
+ * Pins the UMMA descriptors, the swizzle and the TMA tensor maps. */
+int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t N, int32_t mode,
+                      void* stream);
+
+/* Diagnostic: route per-phase clock64() stamps of the tensor-core ReFT
+ * kernel's first CTA (8 stamps x 16 tiles, device buffer, NULL = off) and
+ * return the cluster count of the last launch. */
+int preft_diag_reft_tc(long long* device_buffer);
 
 /* library / device introspection */
 int preft_abi_version(void);

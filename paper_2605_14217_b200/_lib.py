@@ -98,6 +98,7 @@ SIGNATURES = {
             ctypes.POINTER(PreftMeta),
             ctypes.c_void_p,
             ctypes.c_int64,
+            ctypes.c_int64,
             ctypes.c_int32,
             ctypes.c_void_p,
             ctypes.c_void_p,
@@ -110,6 +111,7 @@ SIGNATURES = {
         ],
     ),
     "preft_set_reft_variant": (ctypes.c_int, [ctypes.c_int32]),
+    "preft_diag_reft_tc": (ctypes.c_int, [ctypes.c_void_p]),
     "preft_convert_2d": (
         ctypes.c_int,
         [
@@ -148,6 +150,7 @@ SIGNATURES = {
             ctypes.c_void_p,
             ctypes.c_void_p,
             ctypes.c_int64,
+            ctypes.c_int64,
             ctypes.c_int32,
             ctypes.c_void_p,
             ctypes.c_void_p,
@@ -169,7 +172,8 @@ SIGNATURES = {
     "preft_set_lora_variant": (ctypes.c_int, [ctypes.c_int32]),
     "preft_tc_selftest": (
         ctypes.c_int,
-        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_void_p],
+        [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+         ctypes.c_void_p],
     ),
     "preft_abi_version": (ctypes.c_int, []),
     "preft_status_string": (ctypes.c_char_p, [ctypes.c_int]),

@@ -11,10 +11,12 @@ namespace preft {
 int meta_build(const preft_meta_t* m, cudaStream_t stream, int num_sms);
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
                int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
-int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
+int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A, const void* B,
                const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
                int num_sms);
 void set_reft_variant(int v);
+void reft_tc_set_profile(long long* buf);
+int reft_tc_last_clusters();
 
 static thread_local char g_last_cuda_error[256] = "";
 
@@ -63,7 +65,7 @@ int grid_for(const void* fn, int threads, int num_sms) {
 }
 
 void set_lora_variant(int v);
-int tc_selftest(const void* A, const void* B, float* D, int K, int N, cudaStream_t s);
+int tc_selftest(const void* A, const void* B, float* D, int K, int N, int mode, cudaStream_t s);
 int plan_num_sms() { return current_num_sms(); }
 int plan_record_cuda(cudaError_t e) { return record_cuda(e); }
 
@@ -123,8 +125,8 @@ const char* preft_last_cuda_error(void) { return g_last_cuda_error; }
 
 int preft_num_sms(void) { return current_num_sms(); }
 
-int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t N, void* stream) {
-    return finish(tc_selftest(A, B, D, K, N, static_cast<cudaStream_t>(stream)));
+int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t N, int32_t mode, void* stream) {
+    return finish(tc_selftest(A, B, D, K, N, mode, static_cast<cudaStream_t>(stream)));
 }
 
 int preft_set_lora_variant(int32_t variant) {
@@ -154,10 +156,15 @@ int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32
                              current_num_sms()));
 }
 
-int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t ldh, int32_t d, const void* A, const void* B,
+int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ldh, int32_t d, const void* A, const void* B,
                      const void* Bt, const void* bias, const void* scale, int32_t r_max, int32_t dtype, void* stream) {
-    return finish(reft_apply(meta, h, ldh, d, A, B, Bt, bias, scale, r_max, dtype, static_cast<cudaStream_t>(stream),
+    return finish(reft_apply(meta, h, rows, ldh, d, A, B, Bt, bias, scale, r_max, dtype, static_cast<cudaStream_t>(stream),
                              current_num_sms()));
+}
+
+int preft_diag_reft_tc(long long* device_buffer) {
+    reft_tc_set_profile(device_buffer);
+    return reft_tc_last_clusters();
 }
 
 int preft_set_reft_variant(int32_t variant) {

@@ -13,7 +13,7 @@ namespace preft {
 int meta_build(const preft_meta_t* m, cudaStream_t stream, int num_sms);
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
                int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
-int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
+int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A, const void* B,
                const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
                int num_sms);
 int plan_num_sms();
@@ -25,6 +25,7 @@ struct PlanOp {
     int tag;
     const void* x;
     void* h;
+    long long rows;
     long long ld;
     int width;
     int nsites;
@@ -46,7 +47,7 @@ using namespace preft;
 
 static int plan_launch(preft_plan* p, const PlanOp& op, cudaStream_t s, int sms) {
     if (op.kind == 0) return lora_apply(&p->meta, op.x, op.ld, op.width, op.sites, op.nsites, op.r, op.dtype, s, sms);
-    return reft_apply(&p->meta, op.h, op.ld, op.width, op.A, op.B, op.Bt, op.bias, op.scale, op.r, op.dtype, s, sms);
+    return reft_apply(&p->meta, op.h, op.rows, op.ld, op.width, op.A, op.B, op.Bt, op.bias, op.scale, op.r, op.dtype, s, sms);
 }
 
 extern "C" {
@@ -87,7 +88,7 @@ int preft_plan_add_lora(preft_plan* p, const void* x, int64_t ldx, int32_t m, co
     return PREFT_OK;
 }
 
-int preft_plan_add_reft(preft_plan* p, void* h, int64_t ldh, int32_t d, const void* A, const void* B,
+int preft_plan_add_reft(preft_plan* p, void* h, int64_t rows, int64_t ldh, int32_t d, const void* A, const void* B,
                         const void* Bt, const void* bias, const void* scale, int32_t r_max, int32_t dtype,
                         int32_t tag) {
     if (!p) return PREFT_ERR_SHAPE;
@@ -95,6 +96,7 @@ int preft_plan_add_reft(preft_plan* p, void* h, int64_t ldh, int32_t d, const vo
     op.kind = 1;
     op.tag = tag;
     op.h = h;
+    op.rows = rows;
     op.ld = ldh;
     op.width = d;
     op.A = A;

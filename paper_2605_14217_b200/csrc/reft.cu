@@ -181,7 +181,7 @@ static bool aligned16r(const void* p) { return (reinterpret_cast<uintptr_t>(p) &
 
 int grid_for(const void* fn, int threads, int num_sms);
 
-int reft_tc_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* Bt,
+int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A, const void* Bt,
                   const void* bias, const void* scale, int r, cudaStream_t stream);
 
 // -1 automatic (tensor cores when eligible), 0 SIMT only, 1 tensor cores only
@@ -195,7 +195,7 @@ int reft_variant() {
 }
 void set_reft_variant(int v) { g_reft_variant = v; }
 
-int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const void* A, const void* B,
+int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A, const void* B,
                const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
                int num_sms) {
     if (!meta || !h || !A || !B || !bias || !scale || d < 1 || ldh < d) return PREFT_ERR_SHAPE;
@@ -203,7 +203,7 @@ int reft_apply(const preft_meta_t* meta, void* h, long long ldh, int d, const vo
     if (dtype != PREFT_DTYPE_F32 && dtype != PREFT_DTYPE_BF16 && dtype != PREFT_DTYPE_F64) return PREFT_ERR_DOMAIN;
     const int variant = reft_variant();
     if (variant != 0 && Bt && dtype == PREFT_DTYPE_BF16) {
-        const int rc = reft_tc_apply(meta, h, ldh, d, A, Bt, bias, scale, r, stream);
+        const int rc = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream);
         if (rc != PREFT_ERR_SHAPE || variant == 1) return rc;  // launched, failed, or TC forced
     } else if (variant == 1) {
         return PREFT_ERR_SHAPE;

@@ -128,7 +128,7 @@ def apply_reft_(h: torch.Tensor, meta: BatchMeta, pool: AdapterPool, layer: int,
     s = _stream(stream, pool.device)
     meta.set_slot_split(pool.slot_split)
     st = _lib.load().preft_reft_apply(
-        ctypes.byref(meta.c), ctypes.c_void_p(h.data_ptr()), row_stride(h), pool.d_model,
+        ctypes.byref(meta.c), ctypes.c_void_p(h.data_ptr()), h.shape[0], row_stride(h), pool.d_model,
         ctypes.c_void_p(pool.reft_A[layer].data_ptr()), ctypes.c_void_p(pool.reft_B[layer].data_ptr()),
         ctypes.c_void_p(pool.reft_Bt[layer].data_ptr() if pool.reft_Bt is not None else None),
         ctypes.c_void_p(pool.reft_bias[layer].data_ptr()), ctypes.c_void_p(pool.reft_scale[layer].data_ptr()),
@@ -243,7 +243,7 @@ def apply_masked_host(params: AdapterParams, out: np.ndarray, src: np.ndarray | 
         meta = _one_entry_meta(cut, total, dev, 0)  # slot 0 is a ReFT-class slot
         s = torch.cuda.current_stream(dev)
         st = _lib.load().preft_reft_apply(
-            ctypes.byref(meta.c), ctypes.c_void_p(y.data_ptr()), row_stride(y), y.shape[1],
+            ctypes.byref(meta.c), ctypes.c_void_p(y.data_ptr()), y.shape[0], row_stride(y), y.shape[1],
             ctypes.c_void_p(ops.A.data_ptr()), ctypes.c_void_p(ops.B.data_ptr()), None,
             ctypes.c_void_p(ops.bias.data_ptr()),
             ctypes.c_void_p(ops.scale.data_ptr()), ops.R, _lib.DTYPE_F64, ctypes.c_void_p(s.cuda_stream)

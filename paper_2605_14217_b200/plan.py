@@ -76,7 +76,7 @@ class StepPlan:
         pool = self.pool
         _check_act(h, "h", pool.d_model, self.rows, pool.dtype, pool.device)
         st = self.lib.preft_plan_add_reft(
-            self.handle, ctypes.c_void_p(h.data_ptr()), row_stride(h), pool.d_model,
+            self.handle, ctypes.c_void_p(h.data_ptr()), h.shape[0], row_stride(h), pool.d_model,
             ctypes.c_void_p(pool.reft_A[layer].data_ptr()), ctypes.c_void_p(pool.reft_B[layer].data_ptr()),
             ctypes.c_void_p(pool.reft_Bt[layer].data_ptr() if pool.reft_Bt is not None else None),
             ctypes.c_void_p(pool.reft_bias[layer].data_ptr()), ctypes.c_void_p(pool.reft_scale[layer].data_ptr()),
