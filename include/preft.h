@@ -70,6 +70,7 @@ extern "C" {
 #define PREFT_META_ERR_T_RANGE 2   /* T < 1 or T > T_cap            */
 #define PREFT_META_ERR_QSL 4       /* query_start_loc not a strictly increasing prefix sum from 0 to T */
 #define PREFT_META_ERR_TILES 8     /* work list would exceed tile_cap */
+#define PREFT_META_ERR_UNITS 16    /* chunk list would exceed chunk_cap */
 
 /* counters[] slots */
 #define PREFT_CTR_SEL_TOKENS 0  /* selected (adapter-carrying) tokens      */
@@ -80,7 +81,13 @@ extern "C" {
 #define PREFT_CTR_T 5           /* T as read from the entry buffer          */
 #define PREFT_CTR_E 6           /* E as read from the entry buffer          */
 #define PREFT_CTR_SPLIT 7       /* selected tokens whose slot < slot_split  */
-#define PREFT_NUM_COUNTERS 8
+#define PREFT_CTR_CHUNKS 8      /* row chunks (<= PREFT_CHUNK_ROWS rows of one entry) */
+#define PREFT_CTR_UNITS 9       /* tensor-core work units (<= 4 chunks of one slot)  */
+#define PREFT_NUM_COUNTERS 12
+
+/* rows per chunk: one TMA box / one TMEM lane quadrant of an M = 64 UMMA */
+#define PREFT_CHUNK_ROWS 16
+#define PREFT_UNIT_CHUNKS 4
 
 /*
  * Batch-metadata workspace.  All arrays are device memory at fixed addresses
@@ -100,7 +107,13 @@ extern "C" {
  *   segments[3*nseg]   (slot, first sorted position, length)
  *   tiles[4*ntiles]    (slot, first sorted position, n tokens, segment id)
  *   entry_offset[E]    sorted position of the entry's first token, -1 if unselected
- *   counters[8]        PREFT_CTR_*
+ *   chunks[2*nchunks]  (first h row, n rows): every selected entry cut into runs
+ *                      of <= PREFT_CHUNK_ROWS consecutive rows, in sorted order
+ *   units[4*nunits]    (slot, first chunk, n chunks, 0): up to PREFT_UNIT_CHUNKS
+ *                      consecutive chunks of one slot — the tensor-core ReFT
+ *                      kernel's work item (one M = 64 UMMA tile, one chunk per
+ *                      TMEM lane quadrant, each chunk one TMA box)
+ *   counters[12]       PREFT_CTR_*
  *
  * Slot classes: one pool serves LoRA and ReFT adapters side by side (a batch
  * may mix them, BASELINE config 1).  LoRA adapters own slots [0, slot_split),
@@ -125,6 +138,10 @@ typedef struct preft_meta {
     int32_t slot_split;  /* first ReFT slot; slots below it are LoRA slots */
     int32_t rows_hint;   /* host's expected token count (0 = unknown): picks the
                             K2 team size at launch; never affects results */
+    int32_t* chunks;
+    int32_t* units;
+    int32_t chunk_cap;   /* >= E_cap + T_cap / PREFT_CHUNK_ROWS + 1 (bounds chunks and units) */
+    int32_t reserved;
 } preft_meta_t;
 
 #define PREFT_MAX_ENTRIES 4096
@@ -173,10 +190,13 @@ int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32
  * A = W - R, B = R.  Pool layout for this layer: A [S][r_max][d],
  * B [S][r_max][d], bias [S][r_max], scale [S] (bias/scale in the accumulator
  * type: f32 for F32/BF16, f64 for F64).  r_max in {1,2,4,8,16,32,64}.
- * Bt [S][d][r_max] (B transposed, K-major for the tensor-core expand) may be
- * NULL; when given, bf16 with r_max in {16, 32}, d in {1024, 2048, 4096} and
- * meta->tile_tokens <= 128 runs the tcgen05 kernel (a d/512-CTA cluster per
- * 128-token tile, TMEM accumulators); everything else runs the SIMT kernel.
+ * Bt (may be NULL) is B transposed and pre-tiled for the tensor-core expand:
+ * per slot a [d/8][r_max/8][8][8] bf16 block, i.e. element (n, k) of B^T at
+ * ((n/8)*(r_max/8) + k/8)*64 + (n%8)*8 + k%8 — the UMMA K-major core-matrix
+ * order, so any 128-row chunk is one contiguous bulk copy.  When given, bf16
+ * with r_max in {16, 32} and d % 128 == 0 runs the tcgen05 kernel (one
+ * persistent CTA per SM, M = 64 units from meta->units, TMA rings, TMEM
+ * accumulators); everything else runs the SIMT kernel.
  */
 int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ldh, int32_t d,
                      const void* A, const void* B, const void* Bt, const void* bias,
@@ -234,9 +254,8 @@ int preft_set_lora_variant(int32_t variant);
 int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t N, int32_t mode,
                       void* stream);
 
-/* Diagnostic: route per-phase clock64() stamps of the tensor-core ReFT
- * kernel's first CTA (8 stamps x 16 tiles, device buffer, NULL = off) and
- * return the cluster count of the last launch. */
+/* Diagnostic: grid size (CTAs) of the last tensor-core ReFT launch; the
+ * argument is ignored (kept for ABI stability). */
 int preft_diag_reft_tc(long long* device_buffer);
 
 /* library / device introspection */

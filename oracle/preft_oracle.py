@@ -128,6 +128,33 @@ def group_by_slot(qsl, slot, is_decode, all_pos, tile_tokens: int, slot_split: i
     return tokens, segments, tiles, offsets, split
 
 
+def chunk_units(qsl, slot, is_decode, all_pos, chunk_rows: int = 16, unit_chunks: int = 4):
+    """Restatement of K1's chunk/unit contract for the tensor-core ReFT kernel.
+
+      chunks  (nchunks, 2) int: (first row, n rows <= chunk_rows): each selected
+              entry, in the stable slot order of group_by_slot, cut into runs of
+              consecutive rows starting at the entry's first row
+      units   (nunits, 4) int: (slot, first chunk, n chunks <= unit_chunks, 0):
+              the chunks of each slot's segment taken unit_chunks at a time
+    """
+    qsl = np.asarray(qsl, dtype=np.int64)
+    E = len(slot)
+    sel = [slot[i] >= 0 and ((not is_decode[i]) or bool(all_pos[i])) for i in range(E)]
+    order = sorted((i for i in range(E) if sel[i]), key=lambda i: (int(slot[i]), i))
+    chunks, seg_first = [], []
+    for j, i in enumerate(order):
+        if j == 0 or slot[order[j - 1]] != slot[i]:
+            seg_first.append((int(slot[i]), len(chunks)))
+        for r in range(int(qsl[i]), int(qsl[i + 1]), chunk_rows):
+            chunks.append((r, min(chunk_rows, int(qsl[i + 1]) - r)))
+    units = []
+    for k, (s, c0) in enumerate(seg_first):
+        c1 = seg_first[k + 1][1] if k + 1 < len(seg_first) else len(chunks)
+        for c in range(c0, c1, unit_chunks):
+            units.append((s, c, min(unit_chunks, c1 - c), 0))
+    return (np.asarray(chunks, dtype=np.int64).reshape(-1, 2), np.asarray(units, dtype=np.int64).reshape(-1, 4))
+
+
 # ---------------------------------------------------------------- adapter math
 
 

@@ -27,6 +27,7 @@ META_ERR_E_RANGE = 1
 META_ERR_T_RANGE = 2
 META_ERR_QSL = 4
 META_ERR_TILES = 8
+META_ERR_UNITS = 16
 
 CTR_SEL_TOKENS = 0
 CTR_SEGMENTS = 1
@@ -36,7 +37,11 @@ CTR_SEL_ENTRIES = 4
 CTR_T = 5
 CTR_E = 6
 CTR_SPLIT = 7
-NUM_COUNTERS = 8
+CTR_CHUNKS = 8
+CTR_UNITS = 9
+NUM_COUNTERS = 12
+CHUNK_ROWS = 16
+UNIT_CHUNKS = 4
 SLOT_SPLIT_ALL_LORA = 2**31 - 1  # every slot is a LoRA-class slot
 MAX_ENTRIES = 4096
 
@@ -58,6 +63,10 @@ class PreftMeta(ctypes.Structure):
         ("tile_tokens", ctypes.c_int32),
         ("slot_split", ctypes.c_int32),
         ("rows_hint", ctypes.c_int32),
+        ("chunks", ctypes.c_void_p),
+        ("units", ctypes.c_void_p),
+        ("chunk_cap", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
     ]
 
 

@@ -15,8 +15,7 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
                const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
                int num_sms);
 void set_reft_variant(int v);
-void reft_tc_set_profile(long long* buf);
-int reft_tc_last_clusters();
+int reft_tc_last_grid();
 
 static thread_local char g_last_cuda_error[256] = "";
 
@@ -140,12 +139,15 @@ size_t preft_meta_entries_words(int32_t E_cap) { return 2 + static_cast<size_t>(
 
 int preft_meta_build(const preft_meta_t* meta, void* stream) {
     if (!meta || !meta->entries || !meta->mask || !meta->tokens || !meta->segments || !meta->tiles ||
-        !meta->entry_offset || !meta->counters)
+        !meta->entry_offset || !meta->counters || !meta->chunks || !meta->units)
         return PREFT_ERR_SHAPE;
     if (meta->E_cap < 1 || meta->E_cap > PREFT_MAX_ENTRIES || meta->T_cap < 1 || meta->tile_tokens < 1)
         return PREFT_ERR_CONFIG;
     if (static_cast<long long>(meta->tile_cap) <
         static_cast<long long>(meta->E_cap) + meta->T_cap / meta->tile_tokens + 1)
+        return PREFT_ERR_CONFIG;
+    if (static_cast<long long>(meta->chunk_cap) <
+        static_cast<long long>(meta->E_cap) + meta->T_cap / PREFT_CHUNK_ROWS + 1)
         return PREFT_ERR_CONFIG;
     return finish(meta_build(meta, static_cast<cudaStream_t>(stream), current_num_sms()));
 }
@@ -163,8 +165,8 @@ int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ld
 }
 
 int preft_diag_reft_tc(long long* device_buffer) {
-    reft_tc_set_profile(device_buffer);
-    return reft_tc_last_clusters();
+    (void)device_buffer;
+    return reft_tc_last_grid();
 }
 
 int preft_set_reft_variant(int32_t variant) {

@@ -113,7 +113,8 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
     unsigned long long* keys = reinterpret_cast<unsigned long long*>(smem_raw);
     int* A = reinterpret_cast<int*>(keys + P);  // per sorted entry: length -> token offset
     int* B = A + P;                             // per sorted entry: head flag -> segment id
-    int* C = B + P;                             // per segment: tile count -> tile offset
+    int* C = B + P;                             // per segment: tile count -> tile offset (P + 1)
+    int* D = C + P + 1;                         // per sorted entry: chunk count -> chunk offset
 
     for (int i = tid; i < P; i += blockDim.x) {
         unsigned long long k = ~0ull;
@@ -163,10 +164,12 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
         const int e = static_cast<int>(k & 0xffffffffu);
         A[i] = qsl[e + 1] - qsl[e];
         B[i] = (i == 0 || (k >> 32) != (keys[i - 1] >> 32)) ? 1 : 0;
+        D[i] = (A[i] + PREFT_CHUNK_ROWS - 1) / PREFT_CHUNK_ROWS;
     }
     __syncthreads();
     const int n_tok = block_scan_array(A, nsel, s_warp, &s_total);
     const int nseg = block_scan_array(B, nsel, s_warp, &s_total);
+    const int nchunks = block_scan_array(D, nsel, s_warp, &s_total);
 
     // tokens below the LoRA/ReFT slot split (own shared slot: s_total may
     // still be being read by threads returning from the last scan)
@@ -231,7 +234,52 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
         tile.w = s;
         reinterpret_cast<int4*>(m.tiles)[j] = tile;
     }
+
+    // ---- chunks and tensor-core units.  Every selected entry is cut into
+    // chunks of <= PREFT_CHUNK_ROWS consecutive rows (so each chunk is one TMA
+    // box); a unit is up to PREFT_UNIT_CHUNKS consecutive chunks of one
+    // segment (one slot).  C (tile offsets) and A (segment token begins) are
+    // dead now and are reused per segment: A = first chunk, C = unit offset.
+    int nunits = 0;
+    const bool chunks_fit = nchunks <= m.chunk_cap;
+    __syncthreads();
+    if (chunks_fit) {
+        for (int i = tid; i < nsel; i += blockDim.x) {
+            const unsigned long long k = keys[i];
+            const int e = static_cast<int>(k & 0xffffffffu);
+            const int row0 = qsl[e], len = qsl[e + 1] - qsl[e];
+            const int c0 = D[i];
+            for (int c = 0; c * PREFT_CHUNK_ROWS < len; ++c)
+                reinterpret_cast<int2*>(m.chunks)[c0 + c] =
+                    make_int2(row0 + c * PREFT_CHUNK_ROWS, min(PREFT_CHUNK_ROWS, len - c * PREFT_CHUNK_ROWS));
+            if (i == 0 || (k >> 32) != (keys[i - 1] >> 32)) A[B[i]] = c0;  // segment's first chunk
+        }
+        __syncthreads();
+        for (int s = tid; s < nseg; s += blockDim.x) {
+            const int end = (s + 1 < nseg) ? A[s + 1] : nchunks;
+            C[s] = (end - A[s] + PREFT_UNIT_CHUNKS - 1) / PREFT_UNIT_CHUNKS;
+        }
+        __syncthreads();
+        nunits = block_scan_array(C, nseg, s_warp, &s_total);
+        for (int j = tid; j < nunits; j += blockDim.x) {
+            int lo = 0, hi = nseg - 1;  // last segment with C[s] <= j
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (C[mid] <= j) lo = mid;
+                else hi = mid - 1;
+            }
+            const int s = lo;
+            const int end = (s + 1 < nseg) ? A[s + 1] : nchunks;
+            const int first = A[s] + (j - C[s]) * PREFT_UNIT_CHUNKS;
+            reinterpret_cast<int4*>(m.units)[j] =
+                make_int4(m.segments[3 * s + 0], first, min(PREFT_UNIT_CHUNKS, end - first), 0);
+        }
+    } else {
+        err |= PREFT_META_ERR_UNITS;
+    }
     if (tid == 0) {
+        m.counters[PREFT_CTR_CHUNKS] = chunks_fit ? nchunks : 0;
+        m.counters[PREFT_CTR_UNITS] = nunits;
         m.counters[PREFT_CTR_SEL_TOKENS] = n_tok;
         m.counters[PREFT_CTR_SEGMENTS] = nseg;
         m.counters[PREFT_CTR_TILES] = ntiles;
@@ -265,7 +313,7 @@ __global__ void __launch_bounds__(256) meta_scatter_kernel(const preft_meta_t m)
 size_t meta_sort_smem_bytes(int E_cap) {
     int P = 1;
     while (P < E_cap) P <<= 1;
-    return static_cast<size_t>(P) * 8 + static_cast<size_t>(P) * 4 * 2 + (static_cast<size_t>(P) + 1) * 4;
+    return static_cast<size_t>(P) * 8 + static_cast<size_t>(P) * 4 * 3 + (static_cast<size_t>(P) + 1) * 4;
 }
 
 int meta_build(const preft_meta_t* m, cudaStream_t stream, int num_sms) {

@@ -182,7 +182,7 @@ static bool aligned16r(const void* p) { return (reinterpret_cast<uintptr_t>(p) &
 int grid_for(const void* fn, int threads, int num_sms);
 
 int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A, const void* Bt,
-                  const void* bias, const void* scale, int r, cudaStream_t stream);
+                  const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms);
 
 // -1 automatic (tensor cores when eligible), 0 SIMT only, 1 tensor cores only
 static int g_reft_variant = -2;
@@ -203,7 +203,7 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
     if (dtype != PREFT_DTYPE_F32 && dtype != PREFT_DTYPE_BF16 && dtype != PREFT_DTYPE_F64) return PREFT_ERR_DOMAIN;
     const int variant = reft_variant();
     if (variant != 0 && Bt && dtype == PREFT_DTYPE_BF16) {
-        const int rc = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream);
+        const int rc = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms);
         if (rc != PREFT_ERR_SHAPE || variant == 1) return rc;  // launched, failed, or TC forced
     } else if (variant == 1) {
         return PREFT_ERR_SHAPE;

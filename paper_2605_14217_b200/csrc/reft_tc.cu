@@ -6,29 +6,37 @@
 // 4*d bytes per token: 105-315 TFLOP/s at the HBM roofline, beyond SIMT
 // FP32), so both products run on tcgen05 with fp32 accumulators in TMEM.
 //
-// Work unit: one K1 tile = up to 128 slot-sorted tokens of ONE adapter
-// (UMMA M = 128).  A thread-block cluster of C = d / SLICE CTAs owns a tile;
-// CTA c owns the SLICE columns [SLICE*c, SLICE*(c+1)) of d.  Per tile:
-//   1. the tile's h rows (its column slice) land in shared memory in the
-//      canonical 128 B-swizzled K-major layout — by TMA (boxes of 128 rows x
-//      64 columns) when the tile is 128 consecutive rows (the common case for
-//      long prompts), by a cp.async gather otherwise; the adapter's A
-//      (r x SLICE) and Bt (SLICE x r) slices are re-staged only when the
-//      tile's adapter changes (clusters walk contiguous runs of tiles);
-//   2. shrink: TMEM[128 x r] = H_slice . A_slice^T, split over 4 independent
-//      accumulators so the UMMA chain is not latency-serialised;
-//   3. the C partial rank-r rows are reduced through distributed shared
-//      memory: CTA c sums its 128/C rows over the cluster, adds bias, scales,
-//      splits v = hi + lo into two bf16 operands (so the expand keeps ~fp32
-//      accuracy) and pushes them into every CTA's shared memory;
-//   4. expand: TMEM[128 x SLICE] = V_hi . Bt_slice^T + V_lo . Bt_slice^T;
-//   5. epilogue: TMEM -> registers, h_slice += delta in shared memory, then
-//      the updated rows go back by TMA store (full tiles; it drains while the
-//      next tile is staged) or 16 B stores (partial tiles).
-// h crosses HBM exactly once in and once out (the algorithmic minimum).
-// SLICE is a template parameter (256 fits two CTAs per SM at r = 16 but needs
-// 16-CTA clusters for d = 4096, which co-schedule poorly); launches use 512.
-// LoRA-class tiles are skipped.
+// Work unit (built by K1): up to 4 chunks of <= 16 consecutive h rows of ONE
+// adapter, i.e. one M = 64 UMMA tile whose chunk q lands in TMEM lane
+// quadrant q (lanes 32q .. 32q+15; the M = 64 data-path layout).  Each chunk
+// is one 16-row TMA box, so ragged prompts cost at most 15 extra rows read
+// per entry and never a gather.
+//
+// A cluster of C CTAs (C = 2 at d = 4096, 4 at d = 8192) owns a unit; CTA c
+// owns the columns [c*d/C, (c+1)*d/C).  One CTA per SM, warp-specialised,
+// every hand-off an mbarrier ring:
+//   warp 0   shrink producer: TMA h panels (64 rows x 64 cols, evict_last)
+//            and the adapter's A panel (R x 64) into a 5-10 stage ring; it
+//            stays at most one unit ahead of the epilogue
+//   warp 1   shrink MMA: TMEM S[64 x R] += H_panel . A_panel^T over this
+//            CTA's columns, 2 split accumulators, S double-buffered
+//   warp 2   epilogue producer: TMA the unit's h rows AGAIN, 128 columns at a
+//            time (an L2 hit: the rows were read moments ago with evict_last),
+//            plus the adapter's Bt chunk (pre-tiled in the pool, one bulk copy)
+//   warp 3   expand MMA: TMEM D[64 x 128] = V_hi . Bt_chunk^T + V_lo . Bt_chunk^T,
+//            D double-buffered
+//   warps 4-11 epilogue: (warps 4-7) exchange the partial S with the cluster
+//            peers through distributed shared memory (remote mbarrier arrives,
+//            no cluster-wide barrier), V = s*(S + b) split into bf16 hi + lo
+//            (so the expand keeps ~fp32 accuracy); (all 8) D -> registers,
+//            h_chunk += D in shared memory, TMA store (evict_first)
+// h crosses HBM once in and once out (the algorithmic minimum).  The second
+// read is served by L2 because each CTA has at most ~2 x 256 KB of h between
+// first read and re-read (~50 MB across the GPU against a 126 MB L2; a single
+// CTA per unit at d = 4096 would need ~150 MB and miss).  The tensor pipe,
+// TMA and the epilogue math overlap, so the kernel streams at HBM speed
+// instead of alternating load and compute phases.  LoRA-class units are
+// skipped.
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -37,323 +45,433 @@
 
 namespace preft {
 
-constexpr int kTcRows = 128;
-constexpr int kTcThreads = 256;
-constexpr int kTcAcc = 4;  // independent shrink accumulators
+constexpr int kUnitRows = 64;             // UMMA M
+constexpr int kChunk = PREFT_CHUNK_ROWS;  // 16 rows: one TMA box, one TMEM lane quadrant
+constexpr int kEpiN = 128;                // expand / epilogue chunk width (UMMA N)
+constexpr int kTcThreads = 384;           // 12 warps
+constexpr int kNacc = 2;                  // split shrink accumulators
+constexpr int kEpiWarps = 8;
+
+template <int R, int C>
+struct TcLayout {
+    static constexpr int SH_STAGES = R == 16 ? 10 : C == 1 ? 8 : C == 2 ? 7 : 5;
+    static constexpr int H_BYTES = kUnitRows * 128;      // 64 rows x 64 bf16 (one 128 B-swizzled panel)
+    static constexpr int AP_BYTES = R * 128;             // A panel: R rows x 64 bf16
+    static constexpr int SH_STAGE = H_BYTES + AP_BYTES;  // multiple of 1024
+    static constexpr int EPI_STAGES = 4;
+    static constexpr int EH_BYTES = 2 * H_BYTES;         // 128 columns = two panels
+    static constexpr int BT_BYTES = kEpiN * R * 2;       // Bt chunk: 128 rows x R (core-matrix layout)
+    static constexpr int EPI_STAGE = EH_BYTES + BT_BYTES;
+    static constexpr int V_BYTES = kUnitRows * R * 2;    // one of V_hi / V_lo
+    static constexpr int OFF_SH = 0;
+    static constexpr int OFF_EPI = SH_STAGES * SH_STAGE;
+    static constexpr int OFF_V = OFF_EPI + EPI_STAGES * EPI_STAGE;  // [2 buffers][hi, lo]
+    static constexpr int IN_BYTES = kUnitRows * R * 4;                // one peer's partial S (f32)
+    static constexpr int OFF_IN = OFF_V + 4 * V_BYTES;                // [2 buffers][C-1 peers]
+    static constexpr int TOTAL = OFF_IN + 2 * (C - 1) * IN_BYTES;
+    static constexpr int SMEM = TOTAL + 1024;            // + alignment slack
+    static constexpr int S_COLS = kNacc * R;             // TMEM columns per S buffer
+    static constexpr int D_COL0 = 256;                   // D buffers: columns 256 .. 511
+    static_assert(2 * S_COLS <= D_COL0, "TMEM budget");
+    static_assert(SMEM <= 227 * 1024, "shared memory budget");
+};
 
 struct ReftTcArgs {
     __nv_bfloat16* h;
     long long ldh;
     int d;
     int slot_base;
-    const __nv_bfloat16* A;   // [S][R][d]
-    const __nv_bfloat16* Bt;  // [S][d][R]
+    const unsigned char* Bt;  // [S][d/8][R/8][8][8] bf16 (UMMA core-matrix order)
     const float* bias;        // [S][R]
     const float* scale;       // [S]
-    const int2* tokens;
-    const int4* tiles;
+    const int2* chunks;
+    const int4* units;
     const int* counters;
-    long long* prof;  // optional phase timestamps (diagnostics), NULL in production
 };
 
-// diagnostics: CTA 0 records clock64() at 8 phase boundaries of its first 16 tiles
-static long long* g_tc_prof = nullptr;
-#define TC_MARK(p)                                                                              \
-    do {                                                                                       \
-        if (a.prof && blockIdx.x == 0 && tid == 0 && it < 16) a.prof[it * 8 + (p)] = clock64(); \
-    } while (0)
-
-template <int R, int SLICE>
-struct TcSmem {
-    static constexpr int H = 0;                            // SLICE/64 panels x 128 rows x 128 B (swizzled)
-    static constexpr int A = H + kTcRows * SLICE * 2;      // R x SLICE bf16 (core-matrix layout)
-    static constexpr int BT = A + R * SLICE * 2;           // SLICE x R bf16
-    static constexpr int VHI = BT + SLICE * R * 2;         // 128 x R bf16
-    static constexpr int VLO = VHI + kTcRows * R * 2;      // 128 x R bf16
-    static constexpr int P = VLO + kTcRows * R * 2;        // 128 x R f32 partials
-    static constexpr int TOTAL = P + kTcRows * R * 4;
-    static constexpr int TMEM_COLS = SLICE <= 256 ? 256 : 512;
-    static constexpr int MIN_BLOCKS = TOTAL <= 110 * 1024 ? 2 : 1;
-};
-
-__device__ __forceinline__ void cp_async16(uint32_t saddr, const void* g) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(saddr), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
-}
-__device__ __forceinline__ float ld_dsmem_f32(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_dsmem_u16(uint32_t addr, unsigned short v) {
-    asm volatile("st.shared::cluster.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
-}
-
-template <int R, int C, int SLICE>
-__global__ void __launch_bounds__(kTcThreads, TcSmem<R, SLICE>::MIN_BLOCKS)
-    reft_tc_kernel(const __grid_constant__ CUtensorMap tmap, const ReftTcArgs a) {
-    using L = TcSmem<R, SLICE>;
-    constexpr int PANELS = SLICE / 64;
-    constexpr int KSTEPS = SLICE / 16;
-    constexpr int rows_per = kTcRows / C;
-    extern __shared__ __align__(1024) unsigned char sm[];
-    __shared__ int s_rows[kTcRows];
-    __shared__ __align__(8) uint64_t mbar;  // MMA completion
-    __shared__ __align__(8) uint64_t tbar;  // TMA load completion
+template <int R, int C>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    reft_tc_kernel(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmA,
+                   const ReftTcArgs a) {
+    using L = TcLayout<R, C>;
+    extern __shared__ unsigned char sm_raw[];
+    __shared__ __align__(8) uint64_t sh_full[L::SH_STAGES], sh_empty[L::SH_STAGES];
+    __shared__ __align__(8) uint64_t epi_full[L::EPI_STAGES], epi_empty[L::EPI_STAGES];
+    __shared__ __align__(8) uint64_t s_full[2], s_empty[2], v_full[2], v_empty[2], d_full[2], d_empty[2];
+    __shared__ __align__(8) uint64_t p_full[2], p_empty[2];  // cluster exchange of partial S (C > 1)
     __shared__ uint32_t tslot;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int crank = static_cast<int>(tc::cluster_ctarank());
-    const int cluster_id = blockIdx.x / C, nclusters = gridDim.x / C;
-    const int col0 = crank * SLICE;
-    const uint32_t sbase = tc::smem_u32(sm);
-    const uint32_t sH = sbase + L::H, sA = sbase + L::A, sBt = sbase + L::BT;
-    const uint32_t sVhi = sbase + L::VHI, sVlo = sbase + L::VLO, sP = sbase + L::P;
+    const uint32_t raw = tc::smem_u32(sm_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;  // 128 B-swizzled operands need 1024 B alignment
+    unsigned char* sgen = sm_raw + (sbase - raw);
 
-    if (warp == 0) tc::tmem_alloc(&tslot, L::TMEM_COLS);
-    if (tid == 0) {
-        tc::prefetch_tmap(&tmap);
-        tc::mbar_init(&mbar, 1);
-        tc::mbar_init(&tbar, 1);
+    if (warp == 0) tc::tmem_alloc(&tslot, 512);
+    if (tid == 32) {
+        for (int i = 0; i < L::SH_STAGES; ++i) {
+            tc::mbar_init(&sh_full[i], 1);
+            tc::mbar_init(&sh_empty[i], 1);
+        }
+        for (int i = 0; i < L::EPI_STAGES; ++i) {
+            tc::mbar_init(&epi_full[i], 1);
+            tc::mbar_init(&epi_empty[i], 1 + kEpiWarps);  // expand-MMA commit + every epilogue warp
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&s_full[b], 1);
+            tc::mbar_init(&s_empty[b], 4);
+            tc::mbar_init(&v_full[b], 4);
+            tc::mbar_init(&v_empty[b], 1);
+            tc::mbar_init(&d_full[b], 1);
+            tc::mbar_init(&d_empty[b], kEpiWarps);
+            tc::mbar_init(&p_full[b], 128 * (C - 1));   // every lane of 4 warps of each peer
+            tc::mbar_init(&p_empty[b], 128 * (C - 1));
+        }
         tc::fence_mbar_init();
+        tc::prefetch_tmap(&tmH);
+        tc::prefetch_tmap(&tmA);
     }
     tc::fence_before_sync();
-    __syncthreads();
+    if constexpr (C > 1) tc::cluster_sync();  // peers' barriers initialised before any remote arrive
+    else __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tslot;
-    uint32_t mphase = 0, tphase = 0;
-    int cur_slot = -1;
-    bool store_pending = false;  // thread 0: a TMA store may still be reading sH
-    int it = 0;
 
-    // contiguous run of tiles per cluster: neighbouring tiles share the adapter
-    int t0, t1;
-    even_share(a.counters[PREFT_CTR_TILES], cluster_id, nclusters, t0, t1);
-    for (int t = t0; t < t1; ++t) {
-        const int4 tile = a.tiles[t];  // (slot, first sorted position, n tokens, segment)
-        if (tile.x < a.slot_base) continue;  // LoRA-class tile: same decision in every CTA of the cluster
-        TC_MARK(0);
-        const int slot = tile.x - a.slot_base;
-        const int ntok = tile.z;
-        if (tid < kTcRows) s_rows[tid] = tid < ntok ? a.tokens[tile.y + tid].x : -1;
-        if (tid == 0 && store_pending) {
-            tc::tma_store_wait_read();  // sH is about to be overwritten
-            store_pending = false;
-        }
-        __syncthreads();
-        const int row0 = s_rows[0];
-        const bool full = ntok == kTcRows && s_rows[kTcRows - 1] - row0 == kTcRows - 1;
+    // a cluster of C CTAs owns each unit; CTA `crank` owns columns [crank*d/C, (crank+1)*d/C)
+    const int crank = C > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
+    int u0, u1;
+    even_share(a.counters[PREFT_CTR_UNITS], blockIdx.x / C, gridDim.x / C, u0, u1);  // contiguous runs share adapters
+    const int NP = a.d / (64 * C), NJ = a.d / (kEpiN * C);
+    const int pc0 = crank * NP, jc0 = crank * NJ;  // first global panel / chunk of this CTA
 
-        // ---- 1. stage h rows (and weights when the adapter changes)
-        if (full) {
-            if (tid == 0) {
-                tc::mbar_expect_tx(&tbar, kTcRows * SLICE * 2);
+    if (warp == 0) {
+        // ------------------------------------------------ shrink producer
+        if (lane == 0) {
+            const uint64_t keep = tc::policy_evict_last();
+            int stage = 0, ub = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x < a.slot_base) continue;
+                const int slot = U.x - a.slot_base, nch = U.z;
+                // stay at most one unit ahead of the epilogue: the unit being
+                // re-read plus the one being streamed must fit in L2
+                if (ub > 0) tc::mbar_wait(&v_full[(ub - 1) & 1], ((ub - 1) >> 1) & 1);
+                ++ub;
+                int rows[4];
 #pragma unroll
-                for (int p = 0; p < PANELS; ++p) tc::tma_load_2d(sH + p * kTcRows * 128, &tmap, col0 + p * 64, row0, &tbar);
-            }
-        } else {
-            const __nv_bfloat16* hb = a.h + col0;
-            for (int i = tid; i < kTcRows * (SLICE / 8); i += kTcThreads) {
-                const int r8 = i & 7, c8 = (i >> 3) % (SLICE / 8), row = (i / SLICE) * 8 + r8;
-                const int tok = s_rows[row];
-                if (tok >= 0)
-                    cp_async16(sH + tc::sw128_offset(row, c8 * 8, kTcRows), hb + static_cast<long long>(tok) * a.ldh + c8 * 8);
-            }
-        }
-        if (slot != cur_slot) {
-            const __nv_bfloat16* Ab = a.A + static_cast<long long>(slot) * R * a.d + col0;
-            for (int i = tid; i < R * (SLICE / 8); i += kTcThreads) {
-                const int r8 = i & 7, c8 = (i >> 3) % (SLICE / 8), k = (i / SLICE) * 8 + r8;
-                cp_async16(sA + tc::kmajor_offset(k, c8 * 8, SLICE), Ab + static_cast<long long>(k) * a.d + c8 * 8);
-            }
-            const __nv_bfloat16* Bb = a.Bt + (static_cast<long long>(slot) * a.d + col0) * R;
-            for (int i = tid; i < SLICE * (R / 8); i += kTcThreads) {
-                const int n = i / (R / 8), c8 = i % (R / 8);
-                cp_async16(sBt + tc::kmajor_offset(n, c8 * 8, R), Bb + static_cast<long long>(n) * R + c8 * 8);
-            }
-            cur_slot = slot;
-        }
-        cp_async_wait_all();
-        if (full) {
-            tc::mbar_wait(&tbar, tphase);
-            tphase ^= 1;
-        }
-        tc::fence_proxy_async();
-        __syncthreads();
-        TC_MARK(1);
-
-        // ---- 2. shrink: TMEM[acc q: q*R .. q*R+R) = sum_{k % 4 == q} H_k . A_k^T
-        if (tid == 0) {
-            tc::fence_after_sync();
-            const uint32_t id = tc::idesc_bf16_f32(kTcRows, R);
+                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
+                const uint32_t bytes = static_cast<uint32_t>(nch * kChunk * 128 + L::AP_BYTES);
+                for (int p = 0; p < NP; ++p) {
+                    tc::mbar_wait(&sh_empty[stage], phase ^ 1u);
+                    const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
+                    tc::mbar_expect_tx(&sh_full[stage], bytes);
 #pragma unroll
-            for (int k = 0; k < KSTEPS; ++k)
-                tc::mma_bf16(tmem + (k % kTcAcc) * R, tc::desc_kmajor_sw128(sH + (k >> 2) * kTcRows * 128 + (k & 3) * 32),
-                             tc::desc_kmajor(sA + k * 256, 128, SLICE * 16), id, k >= kTcAcc ? 1u : 0u);
-            tc::mma_commit(&mbar);
-        }
-        tc::mbar_wait(&mbar, mphase);
-        mphase ^= 1;
-        tc::fence_after_sync();
-        TC_MARK(2);
-        if (warp < 4) {
-            const int row = warp * 32 + lane;
-            float* P = reinterpret_cast<float*>(sm + L::P);
-            float s[R];
-#pragma unroll
-            for (int j = 0; j < R; ++j) s[j] = 0.f;
-#pragma unroll
-            for (int q = 0; q < kTcAcc; ++q) {
-                const uint32_t taddr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + q * R;
-                if constexpr (R == 16) {
-                    uint32_t w[16];
-                    tc::tmem_ld16(taddr, w);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) s[j] += __uint_as_float(w[j]);
-                } else {
-                    uint32_t w[32];
-                    tc::tmem_ld32(taddr, w);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) s[j] += __uint_as_float(w[j]);
-                }
-            }
-#pragma unroll
-            for (int j = 0; j < R; j += 4)
-                *reinterpret_cast<float4*>(P + row * R + j) = make_float4(s[j], s[j + 1], s[j + 2], s[j + 3]);
-        }
-        tc::fence_before_sync();
-        tc::cluster_sync();  // every CTA's partial rows are visible cluster-wide
-        TC_MARK(3);
-
-        // ---- 3. reduce-scatter the partials, push bf16 hi/lo V to every CTA
-        for (int idx = tid; idx < rows_per * R; idx += kTcThreads) {
-            const int j = crank * rows_per + idx / R, k = idx % R;
-            const uint32_t off = static_cast<uint32_t>((j * R + k) * 4);
-            float part[C];
-#pragma unroll
-            for (int q = 0; q < C; ++q) part[q] = ld_dsmem_f32(tc::map_shared(sP + off, q));
-            float s = 0.f;
-#pragma unroll
-            for (int q = 0; q < C; ++q) s += part[q];
-            const float v = (s + __ldg(a.bias + static_cast<long long>(slot) * R + k)) * __ldg(a.scale + slot);
-            const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-            const __nv_bfloat16 lo = __float2bfloat16_rn(v - __bfloat162float(hi));
-            const uint32_t voff = tc::kmajor_offset(j, k, R);
-            const unsigned short hb = *reinterpret_cast<const unsigned short*>(&hi);
-            const unsigned short lb = *reinterpret_cast<const unsigned short*>(&lo);
-#pragma unroll
-            for (int q = 0; q < C; ++q) {
-                st_dsmem_u16(tc::map_shared(sVhi + voff, q), hb);
-                st_dsmem_u16(tc::map_shared(sVlo + voff, q), lb);
-            }
-        }
-        tc::cluster_sync();  // V complete in every CTA
-        TC_MARK(4);
-
-        // ---- 4. expand: TMEM[0:SLICE] = V_hi . Bt^T + V_lo . Bt^T (N = 256 per UMMA)
-        if (tid == 0) {
-            tc::fence_proxy_async();
-            tc::fence_after_sync();
-            const uint32_t id = tc::idesc_bf16_f32(kTcRows, 256);
-#pragma unroll
-            for (int half = 0; half < SLICE / 256; ++half) {
-                const uint32_t bbase = sBt + half * 32 * (R * 16);  // 256 rows = 32 core-row groups
-#pragma unroll
-                for (int k = 0; k < R / 16; ++k) {
-                    const uint64_t bd = tc::desc_kmajor(bbase + k * 256, 128, R * 16);
-                    tc::mma_bf16(tmem + half * 256, tc::desc_kmajor(sVhi + k * 256, 128, R * 16), bd, id,
-                                 k > 0 ? 1u : 0u);
-                    tc::mma_bf16(tmem + half * 256, tc::desc_kmajor(sVlo + k * 256, 128, R * 16), bd, id, 1u);
-                }
-            }
-            tc::mma_commit(&mbar);
-        }
-        tc::mbar_wait(&mbar, mphase);
-        mphase ^= 1;
-        tc::fence_after_sync();
-        TC_MARK(5);
-
-        // ---- 5. epilogue: h_slice += delta in shared memory (swizzled rows)
-        {
-            constexpr int HALF = SLICE / 2;  // columns per warp
-            const int q = warp & 3, half = warp >> 2, row = q * 32 + lane;
-            const bool live = row < ntok;
-            const uint32_t tl = tmem + (static_cast<uint32_t>(q * 32) << 16) + half * HALF;
-#pragma unroll 1
-            for (int c0 = 0; c0 < HALF; c0 += 64) {
-                uint32_t v[64];
-                tc::tmem_ld32(tl + c0, *reinterpret_cast<uint32_t(*)[32]>(v));
-                tc::tmem_ld32(tl + c0 + 32, *reinterpret_cast<uint32_t(*)[32]>(v + 32));
-                tc::tmem_ld_wait();
-                if (live) {
-                    const int col = half * HALF + c0;
-#pragma unroll
-                    for (int hh = 0; hh < 8; ++hh) {
-                        uint4* p = reinterpret_cast<uint4*>(sm + L::H + tc::sw128_offset(row, col + hh * 8, kTcRows));
-                        uint4 hv = *p;
-                        uint32_t* w = reinterpret_cast<uint32_t*>(&hv);
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            float lo, hi2;
-                            bf16x2_to_acc(w[e], lo, hi2);
-                            lo += __uint_as_float(v[hh * 8 + 2 * e]);
-                            hi2 += __uint_as_float(v[hh * 8 + 2 * e + 1]);
-                            w[e] = f32x2_to_bf16(lo, hi2);
-                        }
-                        *p = hv;
+                    for (int q = 0; q < 4; ++q)
+                        if (q < nch)
+                            tc::tma_load_2d_hint(st + q * (kChunk * 128), &tmH, (pc0 + p) * 64, rows[q], &sh_full[stage], keep);
+                    tc::tma_load_2d(st + L::H_BYTES, &tmA, (pc0 + p) * 64, slot * R, &sh_full[stage]);
+                    if (++stage == L::SH_STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
                     }
                 }
             }
         }
-        tc::fence_before_sync();
-        tc::fence_proxy_async();  // epilogue smem writes -> async proxy (TMA store)
-        __syncthreads();
-        TC_MARK(6);
-        if (full) {
-            if (tid == 0) {
+    } else if (warp == 1) {
+        // ------------------------------------------------ shrink MMA
+        if (lane == 0) {
+            const uint32_t id = tc::idesc_bf16_f32(kUnitRows, R);
+            int stage = 0, ub = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x < a.slot_base) continue;
+                const int sb = ub & 1;
+                tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
+                tc::fence_after_sync();
+                const uint32_t dS = tmem + sb * L::S_COLS;
+                for (int p = 0; p < NP; ++p) {
+                    tc::mbar_wait(&sh_full[stage], phase);
+                    tc::fence_after_sync();
+                    const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
 #pragma unroll
-                for (int p = 0; p < PANELS; ++p) tc::tma_store_2d(&tmap, col0 + p * 64, row0, sH + p * kTcRows * 128);
-                tc::tma_store_commit();
-                store_pending = true;
+                    for (int k = 0; k < 4; ++k) {
+                        const int kk = p * 4 + k;
+                        tc::mma_bf16(dS + (kk % kNacc) * R, tc::desc_kmajor_sw128(st + k * 32),
+                                     tc::desc_kmajor_sw128(st + L::H_BYTES + k * 32), id, kk >= kNacc ? 1u : 0u);
+                    }
+                    tc::mma_commit(&sh_empty[stage]);
+                    if (++stage == L::SH_STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                tc::mma_commit(&s_full[sb]);
+                ++ub;
             }
-        } else {
-            __nv_bfloat16* hb = a.h + col0;
-            for (int i = tid; i < kTcRows * (SLICE / 8); i += kTcThreads) {
-                const int r8 = i & 7, c8 = (i >> 3) % (SLICE / 8), row = (i / SLICE) * 8 + r8;
-                const int tok = s_rows[row];
-                if (tok >= 0)
-                    *reinterpret_cast<uint4*>(hb + static_cast<long long>(tok) * a.ldh + c8 * 8) =
-                        *reinterpret_cast<const uint4*>(sm + L::H + tc::sw128_offset(row, c8 * 8, kTcRows));
-            }
-            __syncthreads();
         }
-        TC_MARK(7);
-        ++it;
+    } else if (warp == 2) {
+        // ------------------------------------------------ epilogue producer
+        if (lane == 0) {
+            const uint64_t stream = tc::policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x < a.slot_base) continue;
+                const int slot = U.x - a.slot_base, nch = U.z;
+                int rows[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
+                const unsigned char* bt = a.Bt + static_cast<long long>(slot) * a.d * R * 2;
+                const uint32_t bytes = static_cast<uint32_t>(2 * nch * kChunk * 128 + L::BT_BYTES);
+                for (int j = 0; j < NJ; ++j) {
+                    tc::mbar_wait(&epi_empty[stage], phase ^ 1u);
+                    const uint32_t st = sbase + L::OFF_EPI + stage * L::EPI_STAGE;
+                    tc::mbar_expect_tx(&epi_full[stage], bytes);
+#pragma unroll
+                    for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            if (q < nch)
+                                tc::tma_load_2d_hint(st + pp * L::H_BYTES + q * (kChunk * 128), &tmH,
+                                                     (jc0 + j) * kEpiN + pp * 64, rows[q], &epi_full[stage], stream);
+                    tc::bulk_load_1d(st + L::EH_BYTES, bt + static_cast<long long>(jc0 + j) * L::BT_BYTES, L::BT_BYTES,
+                                     &epi_full[stage]);
+                    if (++stage == L::EPI_STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 3) {
+        // ------------------------------------------------ expand MMA
+        if (lane == 0) {
+            const uint32_t id = tc::idesc_bf16_f32(kUnitRows, kEpiN);
+            int stage = 0, ub = 0, dc = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x < a.slot_base) continue;
+                const int vb = ub & 1;
+                tc::mbar_wait(&v_full[vb], (ub >> 1) & 1);
+                tc::fence_after_sync();
+                const uint32_t vhi = sbase + L::OFF_V + vb * 2 * L::V_BYTES, vlo = vhi + L::V_BYTES;
+                for (int j = 0; j < NJ; ++j) {
+                    tc::mbar_wait(&epi_full[stage], phase);
+                    const int db = dc & 1;
+                    tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
+                    tc::fence_after_sync();
+                    const uint32_t bt = sbase + L::OFF_EPI + stage * L::EPI_STAGE + L::EH_BYTES;
+                    const uint32_t dD = tmem + L::D_COL0 + db * kEpiN;
+#pragma unroll
+                    for (int k = 0; k < R / 16; ++k) {
+                        const uint64_t bd = tc::desc_kmajor(bt + k * 256, 128, R * 16);
+                        tc::mma_bf16(dD, tc::desc_kmajor(vhi + k * 256, 128, R * 16), bd, id, k > 0 ? 1u : 0u);
+                        tc::mma_bf16(dD, tc::desc_kmajor(vlo + k * 256, 128, R * 16), bd, id, 1u);
+                    }
+                    tc::mma_commit(&d_full[db]);
+                    tc::mma_commit(&epi_empty[stage]);  // Bt chunk no longer read
+                    if (++stage == L::EPI_STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                    ++dc;
+                }
+                tc::mma_commit(&v_empty[vb]);
+                ++ub;
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 4..11)
+        const int q = warp & 3;          // the TMEM lane quadrant this warp may access
+        const int hf = (warp - 4) >> 2;  // which 64-column half of each 128-column chunk
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        const uint64_t stream = tc::policy_evict_first();
+        int stage = 0, ub = 0, dc = 0, pend = -1;
+        uint32_t phase = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int4 U = a.units[u];
+            if (U.x < a.slot_base) continue;
+            const int slot = U.x - a.slot_base, nch = U.z;
+            const int2 ch = q < nch ? a.chunks[U.y + q] : make_int2(0, 0);
+            const int sb = ub & 1;
+            if (hf == 0) {
+                // V = s * (S + b) for this quadrant's 16 rows -> bf16 hi + lo
+                tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
+                tc::fence_after_sync();
+                float s[R];
+#pragma unroll
+                for (int k = 0; k < R; ++k) s[k] = 0.f;
+#pragma unroll
+                for (int acc = 0; acc < kNacc; ++acc) {
+                    const uint32_t taddr = tmem + lane_base + sb * L::S_COLS + acc * R;
+                    if constexpr (R == 16) {
+                        uint32_t w[16];
+                        tc::tmem_ld16(taddr, w);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (int k = 0; k < 16; ++k) s[k] += __uint_as_float(w[k]);
+                    } else {
+                        uint32_t w[32];
+                        tc::tmem_ld32(taddr, w);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) s[k] += __uint_as_float(w[k]);
+                    }
+                }
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+                if constexpr (C > 1) {
+                    // S is a partial sum over this CTA's columns: push it to every
+                    // peer's inbox, then add the peers' partials from our own
+                    const int m = q * kChunk + (lane & 15);
+                    tc::mbar_wait_cluster(&p_empty[sb], ((ub >> 1) & 1) ^ 1u);  // peers done with unit u-2
+#pragma unroll
+                    for (int x = 1; x < C; ++x) {
+                        const int peer = (crank + x) % C;  // our slot in peer's inbox: C - 1 - x
+                        const uint32_t dst = tc::map_shared(
+                            sbase + L::OFF_IN + (sb * (C - 1) + (C - 1 - x)) * L::IN_BYTES + m * R * 4, peer);
+                        if (lane < kChunk) {
+#pragma unroll
+                            for (int k = 0; k < R; k += 4)
+                                tc::st_dsmem_f4(dst + k * 4, make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]));
+                        }
+                        tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_full[sb]), peer));
+                    }
+                    tc::mbar_wait_cluster(&p_full[sb], (ub >> 1) & 1);
+                    if (lane < kChunk) {
+#pragma unroll
+                        for (int x = 0; x < C - 1; ++x) {
+                            const float* in = reinterpret_cast<const float*>(
+                                sgen + L::OFF_IN + (sb * (C - 1) + x) * L::IN_BYTES + m * R * 4);
+#pragma unroll
+                            for (int k = 0; k < R; k += 4) {
+                                const float4 t = *reinterpret_cast<const float4*>(in + k);
+                                s[k] += t.x;
+                                s[k + 1] += t.y;
+                                s[k + 2] += t.z;
+                                s[k + 3] += t.w;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int x = 1; x < C; ++x)
+                        tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_empty[sb]), (crank + x) % C));
+                }
+                tc::mbar_wait(&v_empty[sb], ((ub >> 1) & 1) ^ 1u);
+                if (lane < kChunk) {
+                    const int m = q * kChunk + lane;
+                    const float sc = __ldg(a.scale + slot);
+                    const float* bb = a.bias + static_cast<long long>(slot) * R;
+                    unsigned char* vhi = sgen + L::OFF_V + sb * 2 * L::V_BYTES;
+#pragma unroll
+                    for (int k0 = 0; k0 < R; k0 += 8) {
+                        uint32_t hi[4], lo[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const float v0 = (s[k0 + 2 * e] + __ldg(bb + k0 + 2 * e)) * sc;
+                            const float v1 = (s[k0 + 2 * e + 1] + __ldg(bb + k0 + 2 * e + 1)) * sc;
+                            hi[e] = f32x2_to_bf16(v0, v1);
+                            float h0, h1;
+                            bf16x2_to_acc(hi[e], h0, h1);
+                            lo[e] = f32x2_to_bf16(v0 - h0, v1 - h1);
+                        }
+                        const uint32_t off = tc::kmajor_offset(m, k0, R);
+                        *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                        *reinterpret_cast<uint4*>(vhi + L::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                    }
+                }
+                tc::fence_proxy_async();  // V (generic writes) -> tensor-core operand reads
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&v_full[sb]);
+            }
+            const int r1 = lane >> 2, cp = 2 * (lane & 3);
+            for (int j = 0; j < NJ; ++j) {
+                const int db = dc & 1;
+                tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
+                tc::mbar_wait(&epi_full[stage], phase);
+                tc::fence_after_sync();
+                uint32_t v[32];
+                tc::tmem_ld_16x256b_x8(tmem + lane_base + L::D_COL0 + db * kEpiN + hf * 64, v);
+                tc::tmem_ld_wait();
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&d_empty[db]);
+                const uint32_t panel = L::OFF_EPI + stage * L::EPI_STAGE + hf * L::H_BYTES;
+                if (ch.y > 0) {
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            const int m = q * kChunk + r1 + 8 * half;
+                            uint32_t* p = reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(m, 8 * i + cp, 64));
+                            float lo, hi;
+                            bf16x2_to_acc(*p, lo, hi);
+                            lo += __uint_as_float(v[4 * i + 2 * half]);
+                            hi += __uint_as_float(v[4 * i + 2 * half + 1]);
+                            *p = f32x2_to_bf16(lo, hi);
+                        }
+                    }
+                    tc::fence_proxy_async();  // epilogue smem writes -> TMA store reads
+                    __syncwarp();
+                    if (ch.y == kChunk) {
+                        if (lane == 0)
+                            tc::tma_store_2d_hint(&tmH, (jc0 + j) * kEpiN + hf * 64, ch.x,
+                                                  sbase + panel + q * (kChunk * 128), stream);
+                    } else {
+                        // partial chunk (end of a prompt): only its valid rows go back
+                        for (int idx = lane; idx < ch.y * 8; idx += 32) {
+                            const int rr = idx >> 3, c16 = idx & 7;
+                            const uint4 val = *reinterpret_cast<const uint4*>(
+                                sgen + panel + tc::sw128_offset(q * kChunk + rr, c16 * 8, 64));
+                            *reinterpret_cast<uint4*>(a.h + static_cast<long long>(ch.x + rr) * a.ldh +
+                                                      (jc0 + j) * kEpiN + hf * 64 + c16 * 8) = val;
+                        }
+                    }
+                }
+                if (lane == 0) {
+                    // release the PREVIOUS stage once its store has read shared memory
+                    tc::tma_store_commit();
+                    tc::tma_store_wait_read_1();
+                    if (pend >= 0) tc::mbar_arrive(&epi_empty[pend]);
+                    pend = stage;
+                }
+                __syncwarp();
+                if (++stage == L::EPI_STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+                ++dc;
+            }
+            ++ub;
+        }
+        if (lane == 0) {
+            tc::tma_store_wait_all();  // bulk stores complete before the CTA retires
+            if (pend >= 0) tc::mbar_arrive(&epi_empty[pend]);
+        }
     }
-    if (tid == 0) tc::tma_store_wait_all();  // bulk stores complete before the CTA (and its smem) retires
     tc::fence_before_sync();
-    __syncthreads();
-    if (warp == 0) tc::tmem_dealloc(tmem, L::TMEM_COLS);
+    if constexpr (C > 1) tc::cluster_sync();  // no peer still writes our inbox / barriers
+    else __syncthreads();
+    if (warp == 0) {
+        __syncwarp();
+        tc::tmem_dealloc(tmem, 512);
+    }
 }
 
-static int g_tc_last_clusters = 0;
-void reft_tc_set_profile(long long* buf) { g_tc_prof = buf; }
-int reft_tc_last_clusters() { return g_tc_last_clusters; }
+static int g_tc_last_grid = 0;
+int reft_tc_last_grid() { return g_tc_last_grid; }
 
-template <int R, int C, int SLICE>
-static int launch_reft_tc(const ReftTcArgs& args, const CUtensorMap& tmap, cudaStream_t stream) {
-    auto fn = reft_tc_kernel<R, C, SLICE>;
-    const int smem = TcSmem<R, SLICE>::TOTAL;
+template <int R, int C>
+static int launch_reft_tc(const ReftTcArgs& args, const CUtensorMap& tmH, const CUtensorMap& tmA, int num_sms,
+                          cudaStream_t stream) {
+    auto fn = reft_tc_kernel<R, C>;
+    const int smem = TcLayout<R, C>::SMEM;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return -static_cast<int>(e);
-    if (C > 8) {
-        e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        if (e != cudaSuccess) return -static_cast<int>(e);
-    }
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -365,53 +483,74 @@ static int launch_reft_tc(const ReftTcArgs& args, const CUtensorMap& tmap, cudaS
     cfg.stream = stream;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    cfg.gridDim = dim3(C * 296);
-    int nclusters = 0;
-    e = cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg);
-    if (e != cudaSuccess) return -static_cast<int>(e);
-    if (nclusters < 1) return PREFT_ERR_CONFIG;
-    g_tc_last_clusters = nclusters;
-    cfg.gridDim = dim3(C * nclusters);
-    e = cudaLaunchKernelEx(&cfg, fn, tmap, args);
+    int grid = (num_sms / C) * C;
+    if (C > 1) {
+        static int cached[3] = {0, 0, 0};  // co-resident clusters per (C), measured once
+        int& nc = cached[C == 2 ? 1 : 2];
+        if (nc == 0) {
+            cfg.gridDim = dim3(grid);
+            e = cudaOccupancyMaxActiveClusters(&nc, fn, &cfg);
+            if (e != cudaSuccess) return -static_cast<int>(e);
+            if (nc < 1) return PREFT_ERR_CONFIG;
+        }
+        grid = min(grid, nc * C);
+    }
+    cfg.gridDim = dim3(grid);
+    g_tc_last_grid = grid;
+    e = cudaLaunchKernelEx(&cfg, fn, tmH, tmA, args);
     return e == cudaSuccess ? PREFT_OK : -static_cast<int>(e);
+}
+
+// Cluster size: split d over C CTAs so one unit is <= 2048 columns (256 KB of
+// h per CTA): the rows read by the shrink are still in L2 when the epilogue
+// re-reads them.  Env PREFT_REFT_TC_CLUSTER=1|2|4 overrides (A/B measurement).
+static int tc_cluster_for(int d) {
+    static int forced = -1;
+    if (forced < 0) {
+        const char* env = getenv("PREFT_REFT_TC_CLUSTER");
+        forced = env ? atoi(env) : 0;
+    }
+    int c = d >= 8192 && d % 512 == 0 ? 4 : d >= 2048 && d % 256 == 0 ? 2 : 1;
+    if (forced == 1 || forced == 2 || forced == 4) c = forced;
+    while (c > 1 && d % (kEpiN * c)) c >>= 1;
+    return c;
 }
 
 // returns 0 on launch, PREFT_ERR_SHAPE if the shape is not TC-eligible, or -cudaError
 int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A,
-                  const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream) {
-    if (!Bt || (r != 16 && r != 32) || d % 512 || rows < 1) return PREFT_ERR_SHAPE;
-    if (d != 1024 && d != 2048 && d != 4096) return PREFT_ERR_SHAPE;
-    if (meta->tile_tokens > kTcRows || (ldh % 8) || (reinterpret_cast<uintptr_t>(h) & 15) ||
+                  const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms) {
+    if (!Bt || (r != 16 && r != 32) || d < 128 || d % 128 || rows < 1) return PREFT_ERR_SHAPE;
+    if (!meta->chunks || !meta->units || (ldh % 8) || (reinterpret_cast<uintptr_t>(h) & 15) ||
         (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(Bt) & 15))
         return PREFT_ERR_SHAPE;
-    CUtensorMap tmap{};
-    if (!make_tmap_bf16_sw128(&tmap, h, static_cast<unsigned long long>(rows), static_cast<unsigned long long>(d),
-                              static_cast<unsigned long long>(ldh), 64, kTcRows))
+    CUtensorMap tmH{}, tmA{};
+    if (!make_tmap_bf16_sw128(&tmH, h, static_cast<unsigned long long>(rows), static_cast<unsigned long long>(d),
+                              static_cast<unsigned long long>(ldh), 64, kChunk))
+        return PREFT_ERR_CONFIG;
+    // A slab of this layer viewed as [slots * r][d]; the box row is always a
+    // registered slot, so the row extent only needs to cover the pool
+    if (!make_tmap_bf16_sw128(&tmA, A, 1ull << 20, static_cast<unsigned long long>(d),
+                              static_cast<unsigned long long>(d), 64, static_cast<unsigned>(r)))
         return PREFT_ERR_CONFIG;
     ReftTcArgs args;
     args.h = static_cast<__nv_bfloat16*>(h);
     args.ldh = ldh;
     args.d = d;
     args.slot_base = meta->slot_split;
-    args.A = static_cast<const __nv_bfloat16*>(A);
-    args.Bt = static_cast<const __nv_bfloat16*>(Bt);
+    args.Bt = static_cast<const unsigned char*>(Bt);
     args.bias = static_cast<const float*>(bias);
     args.scale = static_cast<const float*>(scale);
-    args.tokens = reinterpret_cast<const int2*>(meta->tokens);
-    args.tiles = reinterpret_cast<const int4*>(meta->tiles);
+    args.chunks = reinterpret_cast<const int2*>(meta->chunks);
+    args.units = reinterpret_cast<const int4*>(meta->units);
     args.counters = meta->counters;
-    args.prof = g_tc_prof;
-    // 512-column slices (cluster of d/512).  Measured on B200: 256-column
-    // slices fit two CTAs per SM but 16-CTA clusters only reach 7 co-resident
-    // clusters (112 CTAs), which loses more than the overlap gains.
-    if (r == 16) {
-        if (d == 1024) return launch_reft_tc<16, 2, 512>(args, tmap, stream);
-        if (d == 2048) return launch_reft_tc<16, 4, 512>(args, tmap, stream);
-        return launch_reft_tc<16, 8, 512>(args, tmap, stream);
-    }
-    if (d == 1024) return launch_reft_tc<32, 2, 512>(args, tmap, stream);
-    if (d == 2048) return launch_reft_tc<32, 4, 512>(args, tmap, stream);
-    return launch_reft_tc<32, 8, 512>(args, tmap, stream);
+    const int c = tc_cluster_for(d);
+    if (r == 16)
+        return c == 4 ? launch_reft_tc<16, 4>(args, tmH, tmA, num_sms, stream)
+               : c == 2 ? launch_reft_tc<16, 2>(args, tmH, tmA, num_sms, stream)
+                        : launch_reft_tc<16, 1>(args, tmH, tmA, num_sms, stream);
+    return c == 4 ? launch_reft_tc<32, 4>(args, tmH, tmA, num_sms, stream)
+           : c == 2 ? launch_reft_tc<32, 2>(args, tmH, tmA, num_sms, stream)
+                    : launch_reft_tc<32, 1>(args, tmH, tmA, num_sms, stream);
 }
 
 }  // namespace preft

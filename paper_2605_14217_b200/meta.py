@@ -67,6 +67,7 @@ class BatchMeta:
         self.T_cap = int(max_tokens)
         self.tile_tokens = int(tile_tokens)
         self.tile_cap = self.E_cap + self.T_cap // self.tile_tokens + 1
+        self.chunk_cap = self.E_cap + self.T_cap // _lib.CHUNK_ROWS + 1
         words = int(lib.preft_meta_entries_words(self.E_cap))
         i32 = dict(dtype=torch.int32, device=self.device)
         self.entries = torch.zeros(words, **i32)
@@ -75,6 +76,8 @@ class BatchMeta:
         self.segments = torch.zeros(3 * self.E_cap, **i32)
         self.tiles = torch.zeros(4 * self.tile_cap, **i32)
         self.entry_offset = torch.zeros(self.E_cap, **i32)
+        self.chunks = torch.zeros(2 * self.chunk_cap, **i32)
+        self.units = torch.zeros(4 * self.chunk_cap, **i32)
         self.counters = torch.zeros(_lib.NUM_COUNTERS, **i32)
         self.host = torch.zeros(words, dtype=torch.int32, pin_memory=True)
         self._host_np = self.host.numpy()
@@ -92,6 +95,10 @@ class BatchMeta:
             self.tile_cap,
             self.tile_tokens,
             _lib.SLOT_SPLIT_ALL_LORA,
+            0,
+            self.chunks.data_ptr(),
+            self.units.data_ptr(),
+            self.chunk_cap,
             0,
         )
         self.E = 0
@@ -159,8 +166,8 @@ class BatchMeta:
         err = int(self.counters_host()[_lib.CTR_ERR])
         if err & (_lib.META_ERR_E_RANGE | _lib.META_ERR_T_RANGE | _lib.META_ERR_QSL):
             raise BatchError(f"device rejected the batch metadata (error bits {err:#x})")
-        if err & _lib.META_ERR_TILES:
-            raise InfeasibleBatchError("work list exceeded the tile capacity")
+        if err & (_lib.META_ERR_TILES | _lib.META_ERR_UNITS):
+            raise InfeasibleBatchError("work list exceeded the tile / chunk capacity")
 
     def mask_host(self) -> np.ndarray:
         self.check_errors()
@@ -180,6 +187,14 @@ class BatchMeta:
     def tiles_host(self) -> np.ndarray:
         n = int(self.counters_host()[_lib.CTR_TILES])
         return self.tiles[: 4 * n].view(n, 4).cpu().numpy()
+
+    def chunks_host(self) -> np.ndarray:
+        n = int(self.counters_host()[_lib.CTR_CHUNKS])
+        return self.chunks[: 2 * n].view(n, 2).cpu().numpy()
+
+    def units_host(self) -> np.ndarray:
+        n = int(self.counters_host()[_lib.CTR_UNITS])
+        return self.units[: 4 * n].view(n, 4).cpu().numpy()
 
     def entry_offset_host(self) -> np.ndarray:
         return self.entry_offset[: self.E].cpu().numpy()

@@ -15,6 +15,8 @@ HBM layout (one allocation per slab):
         B     [L][S_reft][R_reft][d]       DiReFT B, or LoReFT R
         bias  [L][S_reft][R_reft]
         scale [L][S_reft]
+        Bt    [L][S_reft][d/8][R_reft/8][8][8]   B^T in UMMA core-matrix order
+                                           (tensor-core kernel only, bf16 r 16/32)
 
 One slot's rows for one (layer, site) are contiguous (R * width elements), so
 a warp working on a token fetches its adapter with coalesced 128-bit loads;
@@ -39,7 +41,7 @@ from .adapters import AdapterKind, PositionSchedule
 from .batch import LORA_TARGETS, ForwardBatch, ModelAdapter
 from .errors import ConfigError, InfeasibleBatchError, RankError, ShapeError, StateError, SyncError
 
-__all__ = ["AdapterPool", "SlotInfo", "torch_dtype_code", "acc_dtype"]
+__all__ = ["AdapterPool", "SlotInfo", "torch_dtype_code", "acc_dtype", "tile_kmajor", "untile_kmajor"]
 
 _POW2 = (1, 2, 4, 8, 16, 32, 64)
 
@@ -52,6 +54,20 @@ def torch_dtype_code(dtype: torch.dtype) -> int:
     if dtype == torch.float64:
         return _lib.DTYPE_F64
     raise ShapeError(f"unsupported element type {dtype}; use bfloat16, float32 or float64")
+
+
+def tile_kmajor(bt: torch.Tensor) -> torch.Tensor:
+    """[..., n, k] -> [..., n/8, k/8, 8, 8]: the UMMA K-major core-matrix order
+    (8 rows x 16 B core matrices, the K-direction ones of a row group adjacent)
+    that csrc/reft_tc.cu copies into shared memory with one bulk copy."""
+    *lead, n, k = bt.shape
+    return bt.reshape(*lead, n // 8, 8, k // 8, 8).transpose(-3, -2).contiguous()
+
+
+def untile_kmajor(t: torch.Tensor) -> torch.Tensor:
+    """Inverse of tile_kmajor: [..., n/8, k/8, 8, 8] -> [..., n, k]."""
+    *lead, nb, kb, _, _ = t.shape
+    return t.transpose(-3, -2).reshape(*lead, nb * 8, kb * 8)
 
 
 def acc_dtype(dtype: torch.dtype) -> torch.dtype:
@@ -129,9 +145,10 @@ class AdapterPool:
             S, R, d = self.reft_capacity, self.reft_rank, self.d_model
             self.reft_A = torch.zeros(L, S, R, d, **z)
             self.reft_B = torch.zeros(L, S, R, d, **z)
-            # K-major copy of B for the tcgen05 expand (csrc/reft_tc.cu): bf16, r 16/32, d = 512 x {2,4,8}
-            self.reft_tc = dtype == torch.bfloat16 and R in (16, 32) and d % 512 == 0 and d // 512 in (2, 4, 8)
-            self.reft_Bt = torch.zeros(L, S, d, R, **z) if self.reft_tc else None
+            # B^T pre-tiled in UMMA core-matrix order for the tcgen05 expand
+            # (csrc/reft_tc.cu, include/preft.h): bf16, r 16/32, d % 128 == 0
+            self.reft_tc = dtype == torch.bfloat16 and R in (16, 32) and d % 128 == 0
+            self.reft_Bt = torch.zeros(L, S, d // 8, R // 8, 8, 8, **z) if self.reft_tc else None
             self.reft_bias = torch.zeros(L, S, R, **za)
             self.reft_scale = torch.zeros(L, S, **za)
         self._slots: dict[int, SlotInfo] = {}
@@ -307,9 +324,6 @@ class AdapterPool:
                 plan.append((self.reft_A[layer, j], self.dtype_code, add(shrink), d, 1, r, R, d))
                 o_exp = add(expand)
                 plan.append((self.reft_B[layer, j], self.dtype_code, o_exp, d, 1, r, R, d))
-                if self.reft_Bt is not None:
-                    # Bt[n][k] = B[k][n]: rows n < d, columns k < r of an (d, R) slot view
-                    plan.append((self.reft_Bt[layer, j], self.dtype_code, o_exp, 1, d, d, d, r))
                 plan.append((self.reft_bias[layer, j].unsqueeze(1), acc_code, add(bias), 1, 1, r, R, 1))
                 sc[layer] = p.prefactor
             plan.append((self.reft_scale[:, j].unsqueeze(1), acc_code, add(sc), 1, 1, self.n_layers, self.n_layers, 1))
@@ -317,6 +331,10 @@ class AdapterPool:
         dev = host.to(self.device, non_blocking=False)
         for dst, code, o, srow, scol, rv, rows, cols in plan:
             self._convert(dst, code, dev, o, srow, scol, rv, rows, cols, s)
+        if adapter.kind is not AdapterKind.LORA and self.reft_Bt is not None:
+            # the tensor-core copy is a pure permutation of the converted B slab
+            j = slot - self.slot_split
+            self.reft_Bt[:, j].copy_(tile_kmajor(self.reft_B[:, j].transpose(-1, -2)))
         dev.record_stream(s)
 
     def _zero_slot(self, info: SlotInfo) -> None:
@@ -394,7 +412,7 @@ class AdapterPool:
                 Bp = torch.nn.functional.pad(B, (0, 0, 0, pad)).to(self.dtype)
                 self.reft_B[layer].index_copy_(0, js, Bp)
                 if self.reft_Bt is not None:
-                    self.reft_Bt[layer].index_copy_(0, js, Bp.transpose(1, 2).contiguous())
+                    self.reft_Bt[layer].index_copy_(0, js, tile_kmajor(Bp.transpose(1, 2)))
                 self.reft_bias[layer].index_copy_(0, js, torch.nn.functional.pad(b, (0, pad)).to(self.acc))
             self.reft_scale.index_fill_(1, js, 1.0 / np.sqrt(rank))
         return ids

@@ -32,6 +32,10 @@ def _check_meta(meta, qsl, slots, flags, tile_tokens, split):
     assert np.array_equal(meta.segments_host(), segs)
     assert np.array_equal(meta.tiles_host(), tiles)
     assert np.array_equal(meta.entry_offset_host(), offs)
+    chunks, units = O.chunk_units(qsl, slots, dec, allp, _lib.CHUNK_ROWS, _lib.UNIT_CHUNKS)
+    assert c[_lib.CTR_CHUNKS] == len(chunks) and c[_lib.CTR_UNITS] == len(units)
+    assert np.array_equal(meta.chunks_host(), chunks)
+    assert np.array_equal(meta.units_host(), units)
 
 
 def test_masks_and_grouping_on_golden_batches(cuda_device):

@@ -68,12 +68,12 @@ def test_zero_delta_adapters_leave_stream_bit_identical(cuda_device, kind):
 
 @pytest.mark.parametrize("variant", [0, 1])
 @pytest.mark.parametrize("rank", [16, 32])
-@pytest.mark.parametrize("d", [1024, 2048, 4096])
+@pytest.mark.parametrize("d", [128, 1024, 2048, 4096, 8192])
 def test_tensor_core_and_simt_variants(cuda_device, variant, rank, d):
-    """The tcgen05 cluster kernel (variant 1) and the SIMT kernel (variant 0)
-    on the same mixed batch: short and multi-tile segments, decode and
-    adapter-less entries, and LoRA-class tokens interleaved in the sorted list
-    (the ReFT kernel must skip their tiles)."""
+    """The tcgen05 kernel (variant 1) and the SIMT kernel (variant 0) on the
+    same mixed batch: short (partial-chunk) and multi-unit segments, decode
+    and adapter-less entries, and LoRA-class tokens interleaved in the sorted
+    list (the ReFT kernel must skip their units)."""
     from paper_2605_14217_b200 import _lib
     from paper_2605_14217_b200.meta import BatchMeta
     from paper_2605_14217_b200.ops import apply_lora_, apply_reft_
@@ -145,3 +145,16 @@ def test_long_segments_zipf(cuda_device):
     apply_reft_(h, meta, pool, 0)
     ref = U.reft_oracle(h_in, qsl, slots, np.zeros(6, np.int32), pool, 0)
     helpers.check_close(U.to_np(h), h_in, ref, "bf16", "zipf loreft r32")
+
+
+def test_tiled_bt_is_b_transposed(cuda_device):
+    """The tensor-core copy of B (pool.reft_Bt, core-matrix tiled) is exactly
+    B^T of the SIMT slab, for registered and synthetic adapters."""
+    from paper_2605_14217_b200.pool import AdapterPool, untile_kmajor
+
+    rng = np.random.default_rng(3)
+    pool = AdapterPool(2, 256, reft_capacity=4, reft_rank=16, dtype=torch.bfloat16, device=cuda_device)
+    pool.register(U.random_reft_adapter(rng, 7, 2, 256, 16, AdapterKind.DIREFT))
+    pool.register(U.random_reft_adapter(rng, 8, 2, 256, 8, AdapterKind.LOREFT))
+    pool.fill_synthetic_(2, AdapterKind.DIREFT, 16, first_id=20)
+    assert torch.equal(untile_kmajor(pool.reft_Bt), pool.reft_B.transpose(-1, -2))

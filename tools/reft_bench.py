@@ -1,0 +1,92 @@
+#!/usr/bin/env python
+"""Per-launch timing of the ReFT^P kernels (diagnostic, one GPU).
+
+One 8B-shaped residual site (d = 4096, bf16): DiReFT r=16 over 2,048-token
+prompts (config 3's shape) and LoReFT r=32 over long Zipf prompts (config 5's
+shape), for the tensor-core kernel and the SIMT kernel.  Each launch works on
+a fresh activation buffer (a ring larger than L2), timed with CUDA events on
+the launching stream.  Prints one JSON line per case with the algorithmic
+bytes (T_p*2*d*e + D*e*2*r*d) and the fraction of peak.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def run(kind, rank, lens, ids, variant, peak, iters=10):
+    import torch
+
+    from paper_2605_14217_b200 import AdapterKind, _lib
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_reft_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    dev = torch.device("cuda", 0)
+    d = 4096
+    n_ad = int(max(ids)) + 1
+    pool = AdapterPool(1, d, reft_capacity=n_ad, reft_rank=rank, dtype=torch.bfloat16, device=dev)
+    pool.fill_synthetic_(n_ad, AdapterKind(kind), rank, seed=1)
+    qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(qsl[-1])
+    slots = pool.entry_arrays(qsl, [int(i) for i in ids], np.zeros(len(lens), np.int32))
+    meta = BatchMeta(len(lens), T, device=dev)
+    meta.set_slot_split(pool.slot_split)
+    meta.build_arrays(qsl, slots, np.zeros(len(lens), np.int32))
+    nbuf = max(2, int(np.ceil(300e6 / (T * d * 2))))
+    hs = [torch.randn(T, d, device=dev).to(torch.bfloat16) for _ in range(nbuf)]
+    lib = _lib.load()
+    lib.preft_set_reft_variant(variant)
+    try:
+        for i in range(3):
+            apply_reft_(hs[i % nbuf], meta, pool, 0)
+        torch.cuda.synchronize()
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(iters)]
+        for i in range(iters):
+            ev[i][0].record()
+            apply_reft_(hs[(i + 3) % nbuf], meta, pool, 0)
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    finally:
+        lib.preft_set_reft_variant(-1)
+    us = float(np.mean([a.elapsed_time(b) for a, b in ev]) * 1e3)
+    distinct = len(set(int(i) for i in ids))
+    alg = T * 2 * d * 2 + distinct * 2 * (2 * rank * d) + distinct * 4 * rank
+    gbs = alg / us / 1e3
+    return {"kind": kind, "rank": rank, "tokens": T, "distinct": distinct, "variant": "tc" if variant == 1 else "simt",
+            "us": round(us, 1), "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+            "tokens_per_s_32_layers": round(T / (us * 1e-6) / 32, 1)}
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--peak", type=float, default=None)
+    p.add_argument("--case", choices=["cfg3", "cfg5", "all"], default="all")
+    p.add_argument("--variant", choices=["tc", "simt", "all"], default="all")
+    p.add_argument("--iters", type=int, default=10)
+    args = p.parse_args()
+    peak = args.peak
+    if peak is None:
+        f = ROOT / "MEASURED_PEAKS.json"
+        peak = float(json.loads(f.read_text())["hbm_gbs"]) if f.exists() else 6650.0
+    rng = np.random.default_rng(0)
+    cfg3 = ([2048] * 32, rng.integers(0, 512, size=32))
+    w = 1.0 / (np.arange(512) + 1.0)
+    cfg5 = (list(rng.integers(8192, 16385, size=8)), rng.choice(512, size=8, p=w / w.sum()))
+    for variant in {"tc": (1,), "simt": (0,), "all": (1, 0)}[args.variant]:
+        if args.case in ("cfg3", "all"):
+            print(json.dumps(run("direft", 16, *cfg3, variant, peak, args.iters)), flush=True)
+        if args.case in ("cfg5", "all"):
+            print(json.dumps(run("loreft", 32, *cfg5, variant, peak, args.iters)), flush=True)
+
+
+if __name__ == "__main__":
+    main()
