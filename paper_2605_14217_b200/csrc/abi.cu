@@ -16,6 +16,7 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
                int num_sms);
 void set_reft_variant(int v);
 int reft_tc_last_grid();
+void reft_tc_set_profile(long long* buf);
 
 static thread_local char g_last_cuda_error[256] = "";
 
@@ -165,7 +166,7 @@ int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ld
 }
 
 int preft_diag_reft_tc(long long* device_buffer) {
-    (void)device_buffer;
+    reft_tc_set_profile(device_buffer);
     return reft_tc_last_grid();
 }
 

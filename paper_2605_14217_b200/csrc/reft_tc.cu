@@ -48,21 +48,27 @@ namespace preft {
 constexpr int kUnitRows = 64;             // UMMA M
 constexpr int kChunk = PREFT_CHUNK_ROWS;  // 16 rows: one TMA box, one TMEM lane quadrant
 constexpr int kEpiN = 128;                // expand / epilogue chunk width (UMMA N)
-constexpr int kTcThreads = 384;           // 12 warps
+constexpr int kTcThreads = 512;           // 16 warps
 constexpr int kNacc = 2;                  // split shrink accumulators
 constexpr int kEpiWarps = 8;
 
 template <int R, int C>
 struct TcLayout {
-    static constexpr int SH_STAGES = R == 16 ? 10 : C == 1 ? 8 : C == 2 ? 7 : 5;
     static constexpr int H_BYTES = kUnitRows * 128;      // 64 rows x 64 bf16 (one 128 B-swizzled panel)
     static constexpr int AP_BYTES = R * 128;             // A panel: R rows x 64 bf16
     static constexpr int SH_STAGE = H_BYTES + AP_BYTES;  // multiple of 1024
-    static constexpr int EPI_STAGES = 4;
     static constexpr int EH_BYTES = 2 * H_BYTES;         // 128 columns = two panels
     static constexpr int BT_BYTES = kEpiN * R * 2;       // Bt chunk: 128 rows x R (core-matrix layout)
     static constexpr int EPI_STAGE = EH_BYTES + BT_BYTES;
     static constexpr int V_BYTES = kUnitRows * R * 2;    // one of V_hi / V_lo
+    // the epilogue re-read is an L2 hit (~1.5k cycles) and needs a short
+    // ring; the shrink streams from HBM (~4-5k cycles under load) and gets
+    // every byte left
+    static constexpr int EPI_STAGES = 4;
+    static constexpr int FIXED = EPI_STAGES * EPI_STAGE + 4 * V_BYTES + 2 * (C - 1) * kUnitRows * R * 4 + 1024;
+    static constexpr int SH_FIT = (227 * 1024 - 1024 - FIXED) / SH_STAGE;  // - static smem (barriers)
+    static constexpr int SH_STAGES = SH_FIT > 14 ? 14 : SH_FIT;
+    static_assert(SH_STAGES >= 4, "shrink ring too shallow");
     static constexpr int OFF_SH = 0;
     static constexpr int OFF_EPI = SH_STAGES * SH_STAGE;
     static constexpr int OFF_V = OFF_EPI + EPI_STAGES * EPI_STAGE;  // [2 buffers][hi, lo]
@@ -73,7 +79,7 @@ struct TcLayout {
     static constexpr int S_COLS = kNacc * R;             // TMEM columns per S buffer
     static constexpr int D_COL0 = 256;                   // D buffers: columns 256 .. 511
     static_assert(2 * S_COLS <= D_COL0, "TMEM budget");
-    static_assert(SMEM <= 227 * 1024, "shared memory budget");
+    static_assert(SMEM + 1024 <= 227 * 1024, "shared memory budget (dynamic + static)");
 };
 
 struct ReftTcArgs {
@@ -87,7 +93,18 @@ struct ReftTcArgs {
     const int2* chunks;
     const int4* units;
     const int* counters;
+    int flags;  // diagnostics knobs: bit 0 immediate stage release, bit 1 pace the shrink behind the
+                // epilogue, bit 2 no one-unit throttle of the shrink, bit 3 let the
+                // epilogue producer read ahead of the shrink
+    int look;   // with bit 1: panels the shrink may run ahead of the epilogue's re-read
+    long long* prof;  // diagnostics: clock64 stamps of CTA 0 (NULL in production)
 };
+
+// diagnostics: warp 4 lane 0 of CTA 0 stamps chunk phases (first 64 chunks) and unit phases
+#define PROF(k) \
+    if (a.prof && blockIdx.x == 0 && warp == 4 && lane == 0 && dc < 64) a.prof[dc * 8 + (k)] = clock64()
+#define UPROF(k) \
+    if (a.prof && blockIdx.x == 0 && warp == 12 && lane == 0 && ub < 16) a.prof[512 + ub * 4 + (k)] = clock64()
 
 template <int R, int C>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -100,6 +117,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     __shared__ __align__(8) uint64_t s_full[2], s_empty[2], v_full[2], v_empty[2], d_full[2], d_empty[2];
     __shared__ __align__(8) uint64_t p_full[2], p_empty[2];  // cluster exchange of partial S (C > 1)
     __shared__ uint32_t tslot;
+    __shared__ int s_epi_done;  // epilogue chunks finished (warp 4), read by the shrink producer when pacing
+    __shared__ int s_shrunk;    // h panels landed and consumed by the shrink MMA (monotonic across units)
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t raw = tc::smem_u32(sm_raw);
@@ -108,6 +127,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     if (warp == 0) tc::tmem_alloc(&tslot, 512);
     if (tid == 32) {
+        s_epi_done = 0;
+        s_shrunk = 0;
         for (int i = 0; i < L::SH_STAGES; ++i) {
             tc::mbar_init(&sh_full[i], 1);
             tc::mbar_init(&sh_empty[i], 1);
@@ -118,7 +139,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&s_full[b], 1);
-            tc::mbar_init(&s_empty[b], 4);
+            tc::mbar_init(&s_empty[b], 4);  // the 4 V warps
             tc::mbar_init(&v_full[b], 4);
             tc::mbar_init(&v_empty[b], 1);
             tc::mbar_init(&d_full[b], 1);
@@ -143,10 +164,116 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int NP = a.d / (64 * C), NJ = a.d / (kEpiN * C);
     const int pc0 = crank * NP, jc0 = crank * NJ;  // first global panel / chunk of this CTA
 
-    if (warp == 0) {
+    if (warp >= 12) {
+        // ------------------------------------------------ V warps (12..15): V = s * (S + b) -> bf16 hi + lo
+        const int q = warp & 3;  // the TMEM lane quadrant this warp may access
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        int ub = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int4 U = a.units[u];
+            if (U.x < a.slot_base) continue;
+            const int slot = U.x - a.slot_base;
+            const int sb = ub & 1;
+            // V = s * (S + b) for this quadrant's 16 rows -> bf16 hi + lo
+            tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
+            UPROF(0);
+            tc::fence_after_sync();
+            float s[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) s[k] = 0.f;
+#pragma unroll
+            for (int acc = 0; acc < kNacc; ++acc) {
+                const uint32_t taddr = tmem + lane_base + sb * L::S_COLS + acc * R;
+                if constexpr (R == 16) {
+                    uint32_t w[16];
+                    tc::tmem_ld16(taddr, w);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) s[k] += __uint_as_float(w[k]);
+                } else {
+                    uint32_t w[32];
+                    tc::tmem_ld32(taddr, w);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) s[k] += __uint_as_float(w[k]);
+                }
+            }
+            tc::fence_before_sync();
+            __syncwarp();
+            UPROF(1);
+            if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+            if constexpr (C > 1) {
+                // S is a partial sum over this CTA's columns: push it to every
+                // peer's inbox, then add the peers' partials from our own
+                const int m = q * kChunk + (lane & 15);
+                tc::mbar_wait_cluster(&p_empty[sb], ((ub >> 1) & 1) ^ 1u);  // peers done with unit u-2
+#pragma unroll
+                for (int x = 1; x < C; ++x) {
+                    const int peer = (crank + x) % C;  // our slot in peer's inbox: C - 1 - x
+                    const uint32_t dst = tc::map_shared(
+                        sbase + L::OFF_IN + (sb * (C - 1) + (C - 1 - x)) * L::IN_BYTES + m * R * 4, peer);
+                    if (lane < kChunk) {
+#pragma unroll
+                        for (int k = 0; k < R; k += 4)
+                            tc::st_dsmem_f4(dst + k * 4, make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]));
+                    }
+                    tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_full[sb]), peer));
+                }
+                tc::mbar_wait_cluster(&p_full[sb], (ub >> 1) & 1);
+                if (lane < kChunk) {
+#pragma unroll
+                    for (int x = 0; x < C - 1; ++x) {
+                        const float* in = reinterpret_cast<const float*>(
+                            sgen + L::OFF_IN + (sb * (C - 1) + x) * L::IN_BYTES + m * R * 4);
+#pragma unroll
+                        for (int k = 0; k < R; k += 4) {
+                            const float4 t = *reinterpret_cast<const float4*>(in + k);
+                            s[k] += t.x;
+                            s[k + 1] += t.y;
+                            s[k + 2] += t.z;
+                            s[k + 3] += t.w;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int x = 1; x < C; ++x)
+                    tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_empty[sb]), (crank + x) % C));
+            }
+            tc::mbar_wait(&v_empty[sb], ((ub >> 1) & 1) ^ 1u);
+            UPROF(2);
+            if (lane < kChunk) {
+                const int m = q * kChunk + lane;
+                const float sc = __ldg(a.scale + slot);
+                const float* bb = a.bias + static_cast<long long>(slot) * R;
+                unsigned char* vhi = sgen + L::OFF_V + sb * 2 * L::V_BYTES;
+#pragma unroll
+                for (int k0 = 0; k0 < R; k0 += 8) {
+                    uint32_t hi[4], lo[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float v0 = (s[k0 + 2 * e] + __ldg(bb + k0 + 2 * e)) * sc;
+                        const float v1 = (s[k0 + 2 * e + 1] + __ldg(bb + k0 + 2 * e + 1)) * sc;
+                        hi[e] = f32x2_to_bf16(v0, v1);
+                        float h0, h1;
+                        bf16x2_to_acc(hi[e], h0, h1);
+                        lo[e] = f32x2_to_bf16(v0 - h0, v1 - h1);
+                    }
+                    const uint32_t off = tc::kmajor_offset(m, k0, R);
+                    *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<uint4*>(vhi + L::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                }
+            }
+            tc::fence_proxy_async();  // V (generic writes) -> tensor-core operand reads
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&v_full[sb]);
+            UPROF(3);
+        
+            ++ub;
+        }
+    } else if (warp == 0) {
         // ------------------------------------------------ shrink producer
         if (lane == 0) {
-            const uint64_t keep = tc::policy_evict_last();
+            const uint64_t keep = (a.flags & 16) ? tc::policy_evict_normal() : tc::policy_evict_last();
             int stage = 0, ub = 0;
             uint32_t phase = 0;
             for (int u = u0; u < u1; ++u) {
@@ -155,7 +282,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const int slot = U.x - a.slot_base, nch = U.z;
                 // stay at most one unit ahead of the epilogue: the unit being
                 // re-read plus the one being streamed must fit in L2
-                if (ub > 0) tc::mbar_wait(&v_full[(ub - 1) & 1], ((ub - 1) >> 1) & 1);
+                if (ub > 0 && !(a.flags & 4)) tc::mbar_wait(&v_full[(ub - 1) & 1], ((ub - 1) >> 1) & 1);
                 ++ub;
                 int rows[4];
 #pragma unroll
@@ -163,6 +290,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t bytes = static_cast<uint32_t>(nch * kChunk * 128 + L::AP_BYTES);
                 for (int p = 0; p < NP; ++p) {
                     tc::mbar_wait(&sh_empty[stage], phase ^ 1u);
+                    if ((a.flags & 2) && ub > 1) {
+                        // panel p of this unit may load once the epilogue re-read columns p*64 - look*64 of the previous one
+                        const int need = (ub - 2) * NJ + min(NJ, max(0, (p - a.look) * 64 / kEpiN + 1));
+                        while (*reinterpret_cast<volatile int*>(&s_epi_done) < need) __nanosleep(64);
+                    }
                     const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
                     tc::mbar_expect_tx(&sh_full[stage], bytes);
 #pragma unroll
@@ -192,6 +324,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t dS = tmem + sb * L::S_COLS;
                 for (int p = 0; p < NP; ++p) {
                     tc::mbar_wait(&sh_full[stage], phase);
+                    // these rows are in L2 now: the epilogue producer may re-read them
+                    *reinterpret_cast<volatile int*>(&s_shrunk) = (ub * NP) + p + 1;
+                    if (a.prof && blockIdx.x == 0 && ub < 16 && (p == 0 || p == NP - 1))
+                        a.prof[576 + ub * 2 + (p ? 1 : 0)] = clock64();
                     tc::fence_after_sync();
                     const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
 #pragma unroll
@@ -213,13 +349,15 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     } else if (warp == 2) {
         // ------------------------------------------------ epilogue producer
         if (lane == 0) {
-            const uint64_t stream = tc::policy_evict_first();
-            int stage = 0;
+            const uint64_t stream = (a.flags & 16) ? tc::policy_evict_normal() : tc::policy_evict_first();
+            int stage = 0, ub = 0;
             uint32_t phase = 0;
             for (int u = u0; u < u1; ++u) {
                 const int4 U = a.units[u];
                 if (U.x < a.slot_base) continue;
                 const int slot = U.x - a.slot_base, nch = U.z;
+                const int unit_base = ub * NP;
+                ++ub;
                 int rows[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
@@ -227,6 +365,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t bytes = static_cast<uint32_t>(2 * nch * kChunk * 128 + L::BT_BYTES);
                 for (int j = 0; j < NJ; ++j) {
                     tc::mbar_wait(&epi_empty[stage], phase ^ 1u);
+                    if (!(a.flags & 8)) {
+                        // never re-read columns before the shrink has read them: an
+                        // early (evict_first) epilogue read would miss, and could
+                        // evict the lines before the shrink gets to them
+                        const int need = unit_base + min(NP, (j + 1) * (kEpiN / 64));
+                        while (*reinterpret_cast<volatile int*>(&s_shrunk) < need) __nanosleep(32);
+                    }
                     const uint32_t st = sbase + L::OFF_EPI + stage * L::EPI_STAGE;
                     tc::mbar_expect_tx(&epi_full[stage], bytes);
 #pragma unroll
@@ -260,8 +405,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t vhi = sbase + L::OFF_V + vb * 2 * L::V_BYTES, vlo = vhi + L::V_BYTES;
                 for (int j = 0; j < NJ; ++j) {
                     tc::mbar_wait(&epi_full[stage], phase);
+                    if (a.prof && blockIdx.x == 0 && dc < 64) a.prof[dc * 8 + 0] = clock64();
                     const int db = dc & 1;
                     tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
+                    if (a.prof && blockIdx.x == 0 && dc < 64) a.prof[dc * 8 + 1] = clock64();
                     tc::fence_after_sync();
                     const uint32_t bt = sbase + L::OFF_EPI + stage * L::EPI_STAGE + L::EH_BYTES;
                     const uint32_t dD = tmem + L::D_COL0 + db * kEpiN;
@@ -273,6 +420,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     }
                     tc::mma_commit(&d_full[db]);
                     tc::mma_commit(&epi_empty[stage]);  // Bt chunk no longer read
+                    if (a.prof && blockIdx.x == 0 && dc < 64) a.prof[dc * 8 + 2] = clock64();
                     if (++stage == L::EPI_STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -288,7 +436,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const int q = warp & 3;          // the TMEM lane quadrant this warp may access
         const int hf = (warp - 4) >> 2;  // which 64-column half of each 128-column chunk
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-        const uint64_t stream = tc::policy_evict_first();
+        const uint64_t stream = (a.flags & 16) ? tc::policy_evict_normal() : tc::policy_evict_first();
         int stage = 0, ub = 0, dc = 0, pend = -1;
         uint32_t phase = 0;
         for (int u = u0; u < u1; ++u) {
@@ -297,102 +445,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             const int slot = U.x - a.slot_base, nch = U.z;
             const int2 ch = q < nch ? a.chunks[U.y + q] : make_int2(0, 0);
             const int sb = ub & 1;
-            if (hf == 0) {
-                // V = s * (S + b) for this quadrant's 16 rows -> bf16 hi + lo
-                tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
-                tc::fence_after_sync();
-                float s[R];
-#pragma unroll
-                for (int k = 0; k < R; ++k) s[k] = 0.f;
-#pragma unroll
-                for (int acc = 0; acc < kNacc; ++acc) {
-                    const uint32_t taddr = tmem + lane_base + sb * L::S_COLS + acc * R;
-                    if constexpr (R == 16) {
-                        uint32_t w[16];
-                        tc::tmem_ld16(taddr, w);
-                        tc::tmem_ld_wait();
-#pragma unroll
-                        for (int k = 0; k < 16; ++k) s[k] += __uint_as_float(w[k]);
-                    } else {
-                        uint32_t w[32];
-                        tc::tmem_ld32(taddr, w);
-                        tc::tmem_ld_wait();
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) s[k] += __uint_as_float(w[k]);
-                    }
-                }
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
-                if constexpr (C > 1) {
-                    // S is a partial sum over this CTA's columns: push it to every
-                    // peer's inbox, then add the peers' partials from our own
-                    const int m = q * kChunk + (lane & 15);
-                    tc::mbar_wait_cluster(&p_empty[sb], ((ub >> 1) & 1) ^ 1u);  // peers done with unit u-2
-#pragma unroll
-                    for (int x = 1; x < C; ++x) {
-                        const int peer = (crank + x) % C;  // our slot in peer's inbox: C - 1 - x
-                        const uint32_t dst = tc::map_shared(
-                            sbase + L::OFF_IN + (sb * (C - 1) + (C - 1 - x)) * L::IN_BYTES + m * R * 4, peer);
-                        if (lane < kChunk) {
-#pragma unroll
-                            for (int k = 0; k < R; k += 4)
-                                tc::st_dsmem_f4(dst + k * 4, make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]));
-                        }
-                        tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_full[sb]), peer));
-                    }
-                    tc::mbar_wait_cluster(&p_full[sb], (ub >> 1) & 1);
-                    if (lane < kChunk) {
-#pragma unroll
-                        for (int x = 0; x < C - 1; ++x) {
-                            const float* in = reinterpret_cast<const float*>(
-                                sgen + L::OFF_IN + (sb * (C - 1) + x) * L::IN_BYTES + m * R * 4);
-#pragma unroll
-                            for (int k = 0; k < R; k += 4) {
-                                const float4 t = *reinterpret_cast<const float4*>(in + k);
-                                s[k] += t.x;
-                                s[k + 1] += t.y;
-                                s[k + 2] += t.z;
-                                s[k + 3] += t.w;
-                            }
-                        }
-                    }
-#pragma unroll
-                    for (int x = 1; x < C; ++x)
-                        tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_empty[sb]), (crank + x) % C));
-                }
-                tc::mbar_wait(&v_empty[sb], ((ub >> 1) & 1) ^ 1u);
-                if (lane < kChunk) {
-                    const int m = q * kChunk + lane;
-                    const float sc = __ldg(a.scale + slot);
-                    const float* bb = a.bias + static_cast<long long>(slot) * R;
-                    unsigned char* vhi = sgen + L::OFF_V + sb * 2 * L::V_BYTES;
-#pragma unroll
-                    for (int k0 = 0; k0 < R; k0 += 8) {
-                        uint32_t hi[4], lo[4];
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const float v0 = (s[k0 + 2 * e] + __ldg(bb + k0 + 2 * e)) * sc;
-                            const float v1 = (s[k0 + 2 * e + 1] + __ldg(bb + k0 + 2 * e + 1)) * sc;
-                            hi[e] = f32x2_to_bf16(v0, v1);
-                            float h0, h1;
-                            bf16x2_to_acc(hi[e], h0, h1);
-                            lo[e] = f32x2_to_bf16(v0 - h0, v1 - h1);
-                        }
-                        const uint32_t off = tc::kmajor_offset(m, k0, R);
-                        *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                        *reinterpret_cast<uint4*>(vhi + L::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                    }
-                }
-                tc::fence_proxy_async();  // V (generic writes) -> tensor-core operand reads
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&v_full[sb]);
-            }
             const int r1 = lane >> 2, cp = 2 * (lane & 3);
             for (int j = 0; j < NJ; ++j) {
                 const int db = dc & 1;
                 tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
+                PROF(3);
                 tc::mbar_wait(&epi_full[stage], phase);
+                PROF(4);
                 tc::fence_after_sync();
                 uint32_t v[32];
                 tc::tmem_ld_16x256b_x8(tmem + lane_base + L::D_COL0 + db * kEpiN + hf * 64, v);
@@ -400,23 +459,38 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&d_empty[db]);
+                PROF(5);
                 const uint32_t panel = L::OFF_EPI + stage * L::EPI_STAGE + hf * L::H_BYTES;
                 if (ch.y > 0) {
+                    // all 16 loads first, then the math, then the stores (the
+                    // addresses are disjoint but not provably so to the compiler)
+                    uint32_t hv[16];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) {
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half)
+                            hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
+                                sgen + panel + tc::sw128_offset(q * kChunk + r1 + 8 * half, 8 * i + cp, 64));
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
 #pragma unroll
                         for (int half = 0; half < 2; ++half) {
-                            const int m = q * kChunk + r1 + 8 * half;
-                            uint32_t* p = reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(m, 8 * i + cp, 64));
                             float lo, hi;
-                            bf16x2_to_acc(*p, lo, hi);
+                            bf16x2_to_acc(hv[2 * i + half], lo, hi);
                             lo += __uint_as_float(v[4 * i + 2 * half]);
                             hi += __uint_as_float(v[4 * i + 2 * half + 1]);
-                            *p = f32x2_to_bf16(lo, hi);
+                            hv[2 * i + half] = f32x2_to_bf16(lo, hi);
                         }
-                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half)
+                            *reinterpret_cast<uint32_t*>(sgen + panel +
+                                                         tc::sw128_offset(q * kChunk + r1 + 8 * half, 8 * i + cp, 64)) =
+                                hv[2 * i + half];
                     tc::fence_proxy_async();  // epilogue smem writes -> TMA store reads
                     __syncwarp();
+                    PROF(6);
                     if (ch.y == kChunk) {
                         if (lane == 0)
                             tc::tma_store_2d_hint(&tmH, (jc0 + j) * kEpiN + hf * 64, ch.x,
@@ -435,11 +509,18 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (lane == 0) {
                     // release the PREVIOUS stage once its store has read shared memory
                     tc::tma_store_commit();
-                    tc::tma_store_wait_read_1();
-                    if (pend >= 0) tc::mbar_arrive(&epi_empty[pend]);
-                    pend = stage;
+                    if (a.flags & 1) {
+                        tc::tma_store_wait_read();
+                        tc::mbar_arrive(&epi_empty[stage]);
+                    } else {
+                        tc::tma_store_wait_read_1();
+                        if (pend >= 0) tc::mbar_arrive(&epi_empty[pend]);
+                        pend = stage;
+                    }
+                    if (warp == 4) *reinterpret_cast<volatile int*>(&s_epi_done) = s_epi_done + 1;
                 }
                 __syncwarp();
+                PROF(7);
                 if (++stage == L::EPI_STAGES) {
                     stage = 0;
                     phase ^= 1u;
@@ -463,7 +544,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 static int g_tc_last_grid = 0;
+static long long* g_tc_prof = nullptr;
 int reft_tc_last_grid() { return g_tc_last_grid; }
+void reft_tc_set_profile(long long* buf) { g_tc_prof = buf; }
 
 template <int R, int C>
 static int launch_reft_tc(const ReftTcArgs& args, const CUtensorMap& tmH, const CUtensorMap& tmA, int num_sms,
@@ -543,6 +626,19 @@ int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long l
     args.chunks = reinterpret_cast<const int2*>(meta->chunks);
     args.units = reinterpret_cast<const int4*>(meta->units);
     args.counters = meta->counters;
+    {
+        static int flags = -1, look = 0;
+        if (flags < 0) {
+            const char* f = getenv("PREFT_REFT_TC_FLAGS");
+            const char* l = getenv("PREFT_REFT_TC_LOOK");
+            flags = f ? atoi(f) : 7;  // immediate stage release, shrink paced by the epilogue, no unit throttle
+            look = l ? atoi(l) : -1;
+        }
+        args.flags = flags;
+        // the shrink may run 3/4 of a unit ahead of the epilogue's re-read
+        args.look = look >= 0 ? look : (d / 64) / tc_cluster_for(d) * 3 / 4;
+        args.prof = g_tc_prof;
+    }
     const int c = tc_cluster_for(d);
     if (r == 16)
         return c == 4 ? launch_reft_tc<16, 4>(args, tmH, tmA, num_sms, stream)

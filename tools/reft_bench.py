@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def run(kind, rank, lens, ids, variant, peak, iters=10):
+def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False):
     import torch
 
     from paper_2605_14217_b200 import AdapterKind, _lib
@@ -58,6 +58,30 @@ def run(kind, rank, lens, ids, variant, peak, iters=10):
     finally:
         lib.preft_set_reft_variant(-1)
     us = float(np.mean([a.elapsed_time(b) for a, b in ev]) * 1e3)
+    if prof and variant == 1:
+        import ctypes
+
+        buf = torch.zeros(608, dtype=torch.int64, device=dev)
+        lib.preft_set_reft_variant(1)
+        lib.preft_diag_reft_tc(ctypes.c_void_p(buf.data_ptr()))
+        apply_reft_(hs[0], meta, pool, 0)
+        torch.cuda.synchronize()
+        lib.preft_diag_reft_tc(None)
+        lib.preft_set_reft_variant(-1)
+        st = buf.cpu().numpy()
+        ch = st[:512].reshape(64, 8).astype(np.int64)
+        un = st[512:576].reshape(16, 4).astype(np.int64)
+        sh = st[576:608].reshape(16, 2).astype(np.int64)
+        t0 = int(un[0, 0])
+        names = ["mma_epi_full", "mma_d_empty", "mma_issued", "ep_d_full", "ep_epi_full", "ep_ldtm", "ep_rmw", "ep_released"]
+        print("chunk timeline (cycles from unit 0 s_full), " + " ".join(names), file=sys.stderr)
+        for c in range(min(40, len(ch))):
+            print(c, " ".join(f"{int(v) - t0:8d}" for v in ch[c]), file=sys.stderr)
+        print("units: s_full, S loaded, exchanged, v_full | shrink first panel, last panel", file=sys.stderr)
+        for u in range(16):
+            if un[u, 0]:
+                print(u, " ".join(f"{int(v) - t0:8d}" for v in un[u]), "|",
+                      " ".join(f"{int(v) - t0:8d}" for v in sh[u]), file=sys.stderr)
     distinct = len(set(int(i) for i in ids))
     alg = T * 2 * d * 2 + distinct * 2 * (2 * rank * d) + distinct * 4 * rank
     gbs = alg / us / 1e3
@@ -72,6 +96,7 @@ def main():
     p.add_argument("--case", choices=["cfg3", "cfg5", "all"], default="all")
     p.add_argument("--variant", choices=["tc", "simt", "all"], default="all")
     p.add_argument("--iters", type=int, default=10)
+    p.add_argument("--prof", action="store_true")
     args = p.parse_args()
     peak = args.peak
     if peak is None:
@@ -83,9 +108,9 @@ def main():
     cfg5 = (list(rng.integers(8192, 16385, size=8)), rng.choice(512, size=8, p=w / w.sum()))
     for variant in {"tc": (1,), "simt": (0,), "all": (1, 0)}[args.variant]:
         if args.case in ("cfg3", "all"):
-            print(json.dumps(run("direft", 16, *cfg3, variant, peak, args.iters)), flush=True)
+            print(json.dumps(run("direft", 16, *cfg3, variant, peak, args.iters, args.prof)), flush=True)
         if args.case in ("cfg5", "all"):
-            print(json.dumps(run("loreft", 32, *cfg5, variant, peak, args.iters)), flush=True)
+            print(json.dumps(run("loreft", 32, *cfg5, variant, peak, args.iters, args.prof)), flush=True)
 
 
 if __name__ == "__main__":
