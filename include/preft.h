@@ -171,6 +171,9 @@ typedef struct preft_lora_site {
     int64_t ldy;
     int32_t n;
     int32_t reserved;
+    const void* Bt_tc; /* NULL, or Bt pre-tiled in UMMA core-matrix order
+                          [S][n/8][r_max/8][8][8] (bf16, r_max 16/32): lets
+                          preft_lora_expand run on tensor cores */
 } preft_lora_site_t;
 
 /*
@@ -183,6 +186,37 @@ typedef struct preft_lora_site {
 int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32_t m,
                      const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
                      int32_t dtype, void* stream);
+
+/*
+ * K2 split at the rank-r intermediate (tensor-parallel LoRA^P, BASELINE
+ * config 4; also the r >= 16 path on one GPU).  With A sharded along the
+ * input dimension and B along the output dimension across a TP group:
+ *
+ *   preft_lora_shrink:  P[t][s*r_max + k] = x[t, :] . A_s[a][k, :]
+ *                       (this rank's partial; P in the accumulator type: f32
+ *                       for BF16/F32, f64 for F64; P is indexed by token row,
+ *                       ldp >= nsites * r_max; rows of unselected tokens are
+ *                       left untouched)
+ *   (caller)            P <- all-reduce-sum of P over the TP group (NCCL)
+ *   preft_lora_expand:  y_s[t, :] += scale_s[a] * P[t][s*r_max ..] . Bt_s[a]
+ *
+ * which together equal preft_lora_apply when the group has one rank
+ * (adapters.py:284-288, model.py:449-451).  x / y_s are this rank's column
+ * slices (pass the pointer of the first owned column with the full leading
+ * dimension).  bf16 with r_max in {16, 32}, m % 64 == 0 (shrink) and
+ * n % 128 == 0 with sites[s].Bt_tc given (expand) run on tcgen05 (M = 64
+ * units from meta->units); everything else on the SIMT path.  `rows` is the
+ * number of allocated rows of x / y (TMA bounds).
+ */
+int preft_lora_shrink(const preft_meta_t* meta, const void* x, int64_t rows, int64_t ldx, int32_t m,
+                      const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype,
+                      void* P, int64_t ldp, void* stream);
+int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int64_t rows,
+                      const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype,
+                      void* stream);
+/* split-kernel variant: -1 automatic, 0 SIMT only, 1 tensor cores only
+ * (PREFT_ERR_SHAPE when ineligible).  Env: PREFT_SPLIT_VARIANT=simt|tc. */
+int preft_set_split_variant(int32_t variant);
 
 /*
  * K3 (h has `rows` allocated rows; TMA bounds): h[t,:] += s_a * ((h[t,:] . A_a^T + b_a) . B_a)   for every selected token

@@ -80,6 +80,7 @@ class PreftLoraSite(ctypes.Structure):
         ("ldy", ctypes.c_int64),
         ("n", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
+        ("Bt_tc", ctypes.c_void_p),
     ]
 
 
@@ -120,6 +121,38 @@ SIGNATURES = {
         ],
     ),
     "preft_set_reft_variant": (ctypes.c_int, [ctypes.c_int32]),
+    "preft_lora_shrink": (
+        ctypes.c_int,
+        [
+            ctypes.POINTER(PreftMeta),
+            ctypes.c_void_p,
+            ctypes.c_int64,
+            ctypes.c_int64,
+            ctypes.c_int32,
+            ctypes.POINTER(PreftLoraSite),
+            ctypes.c_int32,
+            ctypes.c_int32,
+            ctypes.c_int32,
+            ctypes.c_void_p,
+            ctypes.c_int64,
+            ctypes.c_void_p,
+        ],
+    ),
+    "preft_lora_expand": (
+        ctypes.c_int,
+        [
+            ctypes.POINTER(PreftMeta),
+            ctypes.c_void_p,
+            ctypes.c_int64,
+            ctypes.c_int64,
+            ctypes.POINTER(PreftLoraSite),
+            ctypes.c_int32,
+            ctypes.c_int32,
+            ctypes.c_int32,
+            ctypes.c_void_p,
+        ],
+    ),
+    "preft_set_split_variant": (ctypes.c_int, [ctypes.c_int32]),
     "preft_diag_reft_tc": (ctypes.c_int, [ctypes.c_void_p]),
     "preft_convert_2d": (
         ctypes.c_int,

@@ -15,6 +15,12 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
                const void* Bt, const void* bias, const void* scale, int r, int dtype, cudaStream_t stream,
                int num_sms);
 void set_reft_variant(int v);
+void set_split_variant(int v);
+int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
+                const preft_lora_site_t* sites, int nsites, int r, int dtype, void* P, long long ldp,
+                cudaStream_t stream, int num_sms);
+int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long long rows, const preft_lora_site_t* sites,
+                int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
 int reft_tc_last_grid();
 void reft_tc_set_profile(long long* buf);
 
@@ -163,6 +169,25 @@ int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ld
                      const void* Bt, const void* bias, const void* scale, int32_t r_max, int32_t dtype, void* stream) {
     return finish(reft_apply(meta, h, rows, ldh, d, A, B, Bt, bias, scale, r_max, dtype, static_cast<cudaStream_t>(stream),
                              current_num_sms()));
+}
+
+int preft_lora_shrink(const preft_meta_t* meta, const void* x, int64_t rows, int64_t ldx, int32_t m,
+                      const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype, void* P,
+                      int64_t ldp, void* stream) {
+    return finish(lora_shrink(meta, x, rows, ldx, m, sites, nsites, r_max, dtype, P, ldp,
+                              static_cast<cudaStream_t>(stream), current_num_sms()));
+}
+
+int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int64_t rows,
+                      const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype, void* stream) {
+    return finish(lora_expand(meta, P, ldp, rows, sites, nsites, r_max, dtype, static_cast<cudaStream_t>(stream),
+                              current_num_sms()));
+}
+
+int preft_set_split_variant(int32_t variant) {
+    if (variant < -1 || variant > 1) return PREFT_ERR_DOMAIN;
+    set_split_variant(variant);
+    return PREFT_OK;
 }
 
 int preft_diag_reft_tc(long long* device_buffer) {

@@ -1,0 +1,777 @@
+// K2 split in two halves around the rank-r intermediate, for tensor-parallel
+// LoRA^P (BASELINE config 4: Llama-3.1-70B, 8-way TP, r = 16) and for r >= 16
+// on one GPU.
+//
+//   shrink:  P[t, s*R + k]  = sum_c x[t, c] . A_s[a][k, c]            (f32)
+//   (TP)     P <- all-reduce_sum(P) over the tensor-parallel group (NCCL)
+//   expand:  y_s[t, :]     += scale_s[a] * sum_k P[t, s*R + k] . Bt_s[a][k, :]
+//
+// which is the reference's  out[rows] += s * ((X A^T) B^T)  (model.py:449-451,
+// adapters.py:284-288) with X A^T computed as a sum of per-rank partials: each
+// rank holds A sharded along the input dimension m and B along the output
+// dimension n, so the pool shards 8 ways and only T_p x r floats per site
+// cross NVLink.  P is indexed by token row (rows of unselected tokens are
+// never read).
+//
+// Two implementations each:
+//   tcgen05 (bf16, R in {16, 32}, m % 64 == 0, n % 128 == 0): the M = 64 unit
+//     pipeline of the tensor-core ReFT kernel (csrc/reft_tc.cu) cut in half —
+//     shrink: TMA x/A panels -> UMMA -> TMEM -> P rows;  expand: P rows ->
+//     bf16 hi/lo V -> UMMA against the pre-tiled Bt chunk -> TMEM -> y chunk
+//     read-modify-write in shared memory -> TMA store.  One CTA per SM.
+//   SIMT (any dtype / rank, one warp per token row) for everything else.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "tc.cuh"
+#include "tmap.cuh"
+
+namespace preft {
+
+int grid_for(const void* fn, int threads, int num_sms);
+
+struct SplitSite {
+    const void* A;
+    const void* Bt;     // row-major [S][R][n] (SIMT)
+    const void* Bt_tc;  // core-matrix tiled [S][n/8][R/8][8][8] (tensor cores)
+    const void* scale;
+    void* y;
+    long long ldy;
+    int n;
+    int pad;
+};
+
+struct SplitArgs {
+    const void* x;
+    long long ldx;
+    int m;
+    int nsites;
+    SplitSite site[3];
+    void* P;  // [rows][ldp] acc type
+    long long ldp;
+    int slot_base;  // LoRA-class slots are < slot_base (meta->slot_split)
+    int pad;
+    const int2* tokens;
+    const int2* chunks;
+    const int4* units;
+    const int* counters;
+};
+
+// ---------------------------------------------------------------- SIMT halves
+
+template <typename T, bool VEC, int R, int NS, int U>
+__global__ void __launch_bounds__(256) shrink_simt_kernel(const SplitArgs a) {
+    using V = Vec<T, VEC>;
+    using acc_t = typename V::acc_t;
+    constexpr int W = V::W;
+    const int lane = threadIdx.x & 31;
+    const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    int i0, i1;
+    even_share(a.counters[PREFT_CTR_SPLIT], gw, nw, i0, i1);
+    const int mv = a.m / W;
+    for (int i = i0; i < i1; ++i) {
+        const int2 ts = a.tokens[i];
+        const T* __restrict__ xr = static_cast<const T*>(a.x) + static_cast<long long>(ts.x) * a.ldx;
+        acc_t acc[NS][R];
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+            for (int k = 0; k < R; ++k) acc[s][k] = acc_t(0);
+        for (int c0 = lane; c0 < mv; c0 += kWarp * U) {
+            typename V::raw_t xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int c = c0 + kWarp * u;
+                xv[u] = c < mv ? V::ld_stream(xr + static_cast<long long>(c) * W) : V::zero();
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int c = c0 + kWarp * u;
+                if (c < mv) {
+                    acc_t xf[W];
+                    V::to_acc(xv[u], xf);
+#pragma unroll
+                    for (int s = 0; s < NS; ++s) {
+                        const T* As = static_cast<const T*>(a.site[s].A) +
+                                      (static_cast<long long>(ts.y) * R) * a.m + static_cast<long long>(c) * W;
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            acc_t af[W];
+                            V::to_acc(V::ld_weight(As + static_cast<long long>(k) * a.m), af);
+#pragma unroll
+                            for (int j = 0; j < W; ++j) acc[s][k] = macc(xf[j], af[j], acc[s][k]);
+                        }
+                    }
+                }
+            }
+        }
+        acc_t* pr = static_cast<acc_t*>(a.P) + static_cast<long long>(ts.x) * a.ldp;
+#pragma unroll
+        for (int s = 0; s < NS; ++s)
+#pragma unroll
+            for (int k = 0; k < R; ++k) {
+                const acc_t v = warp_sum(acc[s][k]);
+                if (lane == ((s * R + k) & 31)) pr[s * R + k] = v;
+            }
+    }
+}
+
+template <typename T, bool VEC, int R, int NS, int U>
+__global__ void __launch_bounds__(256) expand_simt_kernel(const SplitArgs a) {
+    using V = Vec<T, VEC>;
+    using acc_t = typename V::acc_t;
+    constexpr int W = V::W;
+    const int lane = threadIdx.x & 31;
+    const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+    const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    int i0, i1;
+    even_share(a.counters[PREFT_CTR_SPLIT], gw, nw, i0, i1);
+    for (int i = i0; i < i1; ++i) {
+        const int2 ts = a.tokens[i];
+        const acc_t* pr = static_cast<const acc_t*>(a.P) + static_cast<long long>(ts.x) * a.ldp;
+#pragma unroll
+        for (int s = 0; s < NS; ++s) {
+            const acc_t sc = __ldg(static_cast<const acc_t*>(a.site[s].scale) + ts.y);
+            acc_t v[R];
+#pragma unroll
+            for (int k = 0; k < R; ++k) v[k] = pr[s * R + k] * sc;
+            const int n = a.site[s].n, nv = n / W;
+            T* __restrict__ yr = static_cast<T*>(a.site[s].y) + static_cast<long long>(ts.x) * a.site[s].ldy;
+            const T* Bs = static_cast<const T*>(a.site[s].Bt) + (static_cast<long long>(ts.y) * R) * n;
+            for (int c0 = lane; c0 < nv; c0 += kWarp * U) {
+                typename V::raw_t yv[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = c0 + kWarp * u;
+                    yv[u] = c < nv ? V::ld_rw(yr + static_cast<long long>(c) * W) : V::zero();
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int c = c0 + kWarp * u;
+                    if (c < nv) {
+                        acc_t yf[W], d[W];
+                        V::to_acc(yv[u], yf);
+#pragma unroll
+                        for (int j = 0; j < W; ++j) d[j] = acc_t(0);
+#pragma unroll
+                        for (int k = 0; k < R; ++k) {
+                            acc_t bf[W];
+                            V::to_acc(V::ld_weight(Bs + static_cast<long long>(k) * n + static_cast<long long>(c) * W), bf);
+#pragma unroll
+                            for (int j = 0; j < W; ++j) d[j] = macc(v[k], bf[j], d[j]);
+                        }
+#pragma unroll
+                        for (int j = 0; j < W; ++j) yf[j] += d[j];
+                        V::st(yr + static_cast<long long>(c) * W, yf);
+                    }
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- tcgen05 halves
+
+constexpr int kSpU = 64;                  // unit rows (UMMA M)
+constexpr int kSpChunk = PREFT_CHUNK_ROWS;
+constexpr int kSpN = 128;                 // expand chunk width (UMMA N)
+constexpr int kSpAcc = 2;                 // split shrink accumulators
+
+struct SplitMaps {
+    CUtensorMap x;     // x [rows][m] (this rank's columns), 16-row x 64-col boxes
+    CUtensorMap A[3];  // A_s [S*R][m], R-row x 64-col boxes
+    CUtensorMap y[3];  // y_s [rows][n], 16-row x 64-col boxes
+};
+
+template <int R, int NS>
+struct ShrinkLayout {
+    static constexpr int NSR = NS * R;
+    static constexpr int X_BYTES = kSpU * 128;
+    static constexpr int AP_BYTES = R * 128;
+    static constexpr int STAGE = X_BYTES + NS * AP_BYTES;  // multiple of 1024
+    static constexpr int STAGES_FIT = (227 * 1024 - 2048) / STAGE;
+    static constexpr int STAGES = STAGES_FIT > 16 ? 16 : STAGES_FIT;
+    static constexpr int SMEM = STAGES * STAGE + 1024;
+    static constexpr int TMEM_COLS = 2 * kSpAcc * NSR <= 256 ? 256 : 512;
+};
+
+// warps: 0 TMA producer, 1 UMMA issuer, 2..5 TMEM -> P rows (lane quadrant = warp % 4)
+template <int R, int NS>
+__global__ void __launch_bounds__(192, 1) shrink_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
+    using L = ShrinkLayout<R, NS>;
+    extern __shared__ unsigned char sm_raw[];
+    __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
+    __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbase = (tc::smem_u32(sm_raw) + 1023u) & ~1023u;
+    if (warp == 0) tc::tmem_alloc(&tslot, L::TMEM_COLS);
+    if (tid == 32) {
+        for (int i = 0; i < L::STAGES; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&s_full[b], 1);
+            tc::mbar_init(&s_empty[b], 4);
+        }
+        tc::fence_mbar_init();
+        tc::prefetch_tmap(&maps.x);
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tslot;
+    int u0, u1;
+    even_share(a.counters[PREFT_CTR_UNITS], blockIdx.x, gridDim.x, u0, u1);
+    const int NP = a.m / 64;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t stream = tc::policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x >= a.slot_base) continue;  // ReFT-class unit
+                const int nch = U.z;
+                int rows[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
+                const uint32_t bytes = static_cast<uint32_t>(nch * kSpChunk * 128 + NS * L::AP_BYTES);
+                for (int p = 0; p < NP; ++p) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1u);
+                    const uint32_t st = sbase + stage * L::STAGE;
+                    tc::mbar_expect_tx(&full[stage], bytes);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        if (q < nch) tc::tma_load_2d_hint(st + q * (kSpChunk * 128), &maps.x, p * 64, rows[q], &full[stage], stream);
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+                        tc::tma_load_2d(st + L::X_BYTES + s * L::AP_BYTES, &maps.A[s], p * 64, U.x * R, &full[stage]);
+                    if (++stage == L::STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t id = tc::idesc_bf16_f32(kSpU, R);
+            int stage = 0, ub = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x >= a.slot_base) continue;
+                const int sb = ub & 1;
+                tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
+                tc::fence_after_sync();
+                const uint32_t dS = tmem + sb * kSpAcc * L::NSR;
+                for (int p = 0; p < NP; ++p) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::fence_after_sync();
+                    const uint32_t st = sbase + stage * L::STAGE;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int kk = p * 4 + k;
+                        const uint64_t ad = tc::desc_kmajor_sw128(st + k * 32);
+#pragma unroll
+                        for (int s = 0; s < NS; ++s)
+                            tc::mma_bf16(dS + (kk % kSpAcc) * L::NSR + s * R, ad,
+                                         tc::desc_kmajor_sw128(st + L::X_BYTES + s * L::AP_BYTES + k * 32), id,
+                                         kk >= kSpAcc ? 1u : 0u);
+                    }
+                    tc::mma_commit(&empty[stage]);
+                    if (++stage == L::STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                }
+                tc::mma_commit(&s_full[sb]);
+                ++ub;
+            }
+        }
+    } else {
+        const int q = warp & 3;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        int ub = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int4 U = a.units[u];
+            if (U.x >= a.slot_base) continue;
+            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
+            const int sb = ub & 1;
+            tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
+            tc::fence_after_sync();
+            float s[L::NSR];
+#pragma unroll
+            for (int c = 0; c < L::NSR; ++c) s[c] = 0.f;
+#pragma unroll
+            for (int acc = 0; acc < kSpAcc; ++acc)
+#pragma unroll
+                for (int c0 = 0; c0 < L::NSR; c0 += 16) {
+                    uint32_t w[16];
+                    tc::tmem_ld16(tmem + lane_base + sb * kSpAcc * L::NSR + acc * L::NSR + c0, w);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) s[c0 + c] += __uint_as_float(w[c]);
+                }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+            if (lane < ch.y) {
+                float* pr = static_cast<float*>(a.P) + static_cast<long long>(ch.x + lane) * a.ldp;
+#pragma unroll
+                for (int c = 0; c < L::NSR; c += 4)
+                    *reinterpret_cast<float4*>(pr + c) = make_float4(s[c], s[c + 1], s[c + 2], s[c + 3]);
+            }
+            ++ub;
+        }
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        __syncwarp();
+        tc::tmem_dealloc(tmem, L::TMEM_COLS);
+    }
+}
+
+template <int R, int NS>
+struct ExpandLayout {
+    static constexpr int Y_BYTES = 2 * kSpU * 128;         // 64 rows x 128 cols (two swizzled panels)
+    static constexpr int BT_BYTES = kSpN * R * 2;
+    static constexpr int STAGE = Y_BYTES + BT_BYTES;       // multiple of 1024
+    static constexpr int V_BYTES = kSpU * R * 2;           // one V (hi or lo) of one site
+    static constexpr int OFF_V = 0;                        // [2 buffers][NS sites][hi, lo]
+    static constexpr int OFF_RING = 4 * NS * V_BYTES;      // multiple of 1024
+    static constexpr int STAGES_FIT = (227 * 1024 - 2048 - OFF_RING) / STAGE;
+    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+    static constexpr int SMEM = OFF_RING + STAGES * STAGE + 1024;
+};
+
+// warps: 0 TMA producer, 1 UMMA issuer, 2-3 P rows -> bf16 hi/lo V, 4-11 epilogue
+template <int R, int NS>
+__global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
+    using L = ExpandLayout<R, NS>;
+    extern __shared__ unsigned char sm_raw[];
+    __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
+    __shared__ __align__(8) uint64_t v_full[2], v_empty[2], d_full[2], d_empty[2];
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t raw = tc::smem_u32(sm_raw);
+    const uint32_t sbase = (raw + 1023u) & ~1023u;
+    unsigned char* sgen = sm_raw + (sbase - raw);
+    if (warp == 0) tc::tmem_alloc(&tslot, 256);
+    if (tid == 32) {
+        for (int i = 0; i < L::STAGES; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], 1 + 8);  // MMA commit (Bt read) + 8 epilogue warps (y stored)
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&v_full[b], 2);
+            tc::mbar_init(&v_empty[b], 1);
+            tc::mbar_init(&d_full[b], 1);
+            tc::mbar_init(&d_empty[b], 8);
+        }
+        tc::fence_mbar_init();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tslot;
+    int u0, u1;
+    even_share(a.counters[PREFT_CTR_UNITS], blockIdx.x, gridDim.x, u0, u1);
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t stream = tc::policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x >= a.slot_base) continue;
+                const int nch = U.z;
+                int rows[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
+                const uint32_t bytes = static_cast<uint32_t>(2 * nch * kSpChunk * 128 + L::BT_BYTES);
+#pragma unroll 1
+                for (int s = 0; s < NS; ++s) {
+                    const int NJ = a.site[s].n / kSpN;
+                    const unsigned char* bt =
+                        static_cast<const unsigned char*>(a.site[s].Bt_tc) + static_cast<long long>(U.x) * a.site[s].n * R * 2;
+                    for (int j = 0; j < NJ; ++j) {
+                        tc::mbar_wait(&empty[stage], phase ^ 1u);
+                        const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
+                        tc::mbar_expect_tx(&full[stage], bytes);
+#pragma unroll
+                        for (int pp = 0; pp < 2; ++pp)
+#pragma unroll
+                            for (int q = 0; q < 4; ++q)
+                                if (q < nch)
+                                    tc::tma_load_2d_hint(st + pp * kSpU * 128 + q * (kSpChunk * 128), &maps.y[s],
+                                                         j * kSpN + pp * 64, rows[q], &full[stage], stream);
+                        tc::bulk_load_1d(st + L::Y_BYTES, bt + static_cast<long long>(j) * L::BT_BYTES, L::BT_BYTES,
+                                         &full[stage]);
+                        if (++stage == L::STAGES) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            const uint32_t id = tc::idesc_bf16_f32(kSpU, kSpN);
+            int stage = 0, ub = 0, dc = 0;
+            uint32_t phase = 0;
+            for (int u = u0; u < u1; ++u) {
+                const int4 U = a.units[u];
+                if (U.x >= a.slot_base) continue;
+                const int vb = ub & 1;
+                tc::mbar_wait(&v_full[vb], (ub >> 1) & 1);
+                tc::fence_after_sync();
+#pragma unroll 1
+                for (int s = 0; s < NS; ++s) {
+                    const uint32_t vhi = sbase + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES, vlo = vhi + L::V_BYTES;
+                    const int NJ = a.site[s].n / kSpN;
+                    for (int j = 0; j < NJ; ++j) {
+                        tc::mbar_wait(&full[stage], phase);
+                        const int db = dc & 1;
+                        tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
+                        tc::fence_after_sync();
+                        const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
+                        const uint32_t dD = tmem + db * kSpN;
+#pragma unroll
+                        for (int k = 0; k < R / 16; ++k) {
+                            const uint64_t bd = tc::desc_kmajor(bt + k * 256, 128, R * 16);
+                            tc::mma_bf16(dD, tc::desc_kmajor(vhi + k * 256, 128, R * 16), bd, id, k > 0 ? 1u : 0u);
+                            tc::mma_bf16(dD, tc::desc_kmajor(vlo + k * 256, 128, R * 16), bd, id, 1u);
+                        }
+                        tc::mma_commit(&d_full[db]);
+                        tc::mma_commit(&empty[stage]);
+                        if (++stage == L::STAGES) {
+                            stage = 0;
+                            phase ^= 1u;
+                        }
+                        ++dc;
+                    }
+                }
+                tc::mma_commit(&v_empty[vb]);
+                ++ub;
+            }
+        }
+    } else if (warp < 4) {
+        // P rows -> V = scale * P (bf16 hi + lo), 32 rows per warp
+        int ub = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int4 U = a.units[u];
+            if (U.x >= a.slot_base) continue;
+            const int vb = ub & 1;
+            const int m = (warp - 2) * 32 + lane, q = m >> 4, rr = m & 15;
+            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
+            const bool valid = rr < ch.y;
+            const float* pr = static_cast<const float*>(a.P) + static_cast<long long>(ch.x + rr) * a.ldp;
+            tc::mbar_wait(&v_empty[vb], ((ub >> 1) & 1) ^ 1u);
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                const float sc = __ldg(static_cast<const float*>(a.site[s].scale) + U.x);
+                unsigned char* vhi = sgen + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES;
+#pragma unroll
+                for (int k0 = 0; k0 < R; k0 += 8) {
+                    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
+                    if (valid) {
+                        p0 = *reinterpret_cast<const float4*>(pr + s * R + k0);
+                        p1 = *reinterpret_cast<const float4*>(pr + s * R + k0 + 4);
+                    }
+                    const float v[8] = {p0.x * sc, p0.y * sc, p0.z * sc, p0.w * sc,
+                                        p1.x * sc, p1.y * sc, p1.z * sc, p1.w * sc};
+                    uint32_t hi[4], lo[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        hi[e] = f32x2_to_bf16(v[2 * e], v[2 * e + 1]);
+                        float h0, h1;
+                        bf16x2_to_acc(hi[e], h0, h1);
+                        lo[e] = f32x2_to_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
+                    }
+                    const uint32_t off = tc::kmajor_offset(m, k0, R);
+                    *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                    *reinterpret_cast<uint4*>(vhi + L::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                }
+            }
+            tc::fence_proxy_async();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&v_full[vb]);
+            ++ub;
+        }
+    } else {
+        // epilogue: D -> registers, y chunk += D in shared memory, TMA store
+        const int q = warp & 3, hf = (warp - 4) >> 2;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        const uint64_t stream = tc::policy_evict_first();
+        const int r1 = lane >> 2, cp = 2 * (lane & 3);
+        int stage = 0, dc = 0;
+        uint32_t phase = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int4 U = a.units[u];
+            if (U.x >= a.slot_base) continue;
+            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
+#pragma unroll 1
+            for (int s = 0; s < NS; ++s) {
+                const int NJ = a.site[s].n / kSpN;
+                for (int j = 0; j < NJ; ++j) {
+                    const int db = dc & 1;
+                    tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::fence_after_sync();
+                    uint32_t v[32];
+                    tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpN + hf * 64, v);
+                    tc::tmem_ld_wait();
+                    tc::fence_before_sync();
+                    __syncwarp();
+                    if (lane == 0) tc::mbar_arrive(&d_empty[db]);
+                    const uint32_t panel = L::OFF_RING + stage * L::STAGE + hf * kSpU * 128;
+                    if (ch.y > 0) {
+                        uint32_t hv[16];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int half = 0; half < 2; ++half)
+                                hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
+                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64));
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int half = 0; half < 2; ++half) {
+                                float lo, hi;
+                                bf16x2_to_acc(hv[2 * i + half], lo, hi);
+                                lo += __uint_as_float(v[4 * i + 2 * half]);
+                                hi += __uint_as_float(v[4 * i + 2 * half + 1]);
+                                hv[2 * i + half] = f32x2_to_bf16(lo, hi);
+                            }
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int half = 0; half < 2; ++half)
+                                *reinterpret_cast<uint32_t*>(
+                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64)) =
+                                    hv[2 * i + half];
+                        tc::fence_proxy_async();
+                        __syncwarp();
+                        if (ch.y == kSpChunk) {
+                            if (lane == 0)
+                                tc::tma_store_2d_hint(&maps.y[s], j * kSpN + hf * 64, ch.x,
+                                                      sbase + panel + q * (kSpChunk * 128), stream);
+                        } else {
+                            __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y);
+                            for (int idx = lane; idx < ch.y * 8; idx += 32) {
+                                const int rr = idx >> 3, c16 = idx & 7;
+                                const uint4 val = *reinterpret_cast<const uint4*>(
+                                    sgen + panel + tc::sw128_offset(q * kSpChunk + rr, c16 * 8, 64));
+                                *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * a.site[s].ldy +
+                                                          j * kSpN + hf * 64 + c16 * 8) = val;
+                            }
+                        }
+                    }
+                    if (lane == 0) {
+                        tc::tma_store_commit();
+                        tc::tma_store_wait_read();
+                        tc::mbar_arrive(&empty[stage]);
+                    }
+                    __syncwarp();
+                    if (++stage == L::STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                    ++dc;
+                }
+            }
+        }
+        if (lane == 0) tc::tma_store_wait_all();
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (warp == 0) {
+        __syncwarp();
+        tc::tmem_dealloc(tmem, 256);
+    }
+}
+
+// ---------------------------------------------------------------- dispatch
+
+using SplitFn = void (*)(SplitArgs);
+
+template <typename T, bool VEC, int NS, bool SHRINK>
+SplitFn pick_split_rank(int r) {
+    constexpr int U = VEC ? 4 : 2;
+#define PREFT_SPLIT_CASE(RR)                                                                       \
+    case RR:                                                                                       \
+        if constexpr (NS * RR <= 64)                                                               \
+            return SHRINK ? shrink_simt_kernel<T, VEC, RR, NS, U> : expand_simt_kernel<T, VEC, RR, NS, U>; \
+        else                                                                                       \
+            return nullptr;
+    switch (r) {
+        PREFT_SPLIT_CASE(1)
+        PREFT_SPLIT_CASE(2)
+        PREFT_SPLIT_CASE(4)
+        PREFT_SPLIT_CASE(8)
+        PREFT_SPLIT_CASE(16)
+        PREFT_SPLIT_CASE(32)
+        PREFT_SPLIT_CASE(64)
+        default: return nullptr;
+    }
+#undef PREFT_SPLIT_CASE
+}
+
+template <typename T, bool SHRINK>
+SplitFn pick_split(bool vec, int nsites, int r) {
+    if (nsites == 1) return vec ? pick_split_rank<T, true, 1, SHRINK>(r) : pick_split_rank<T, false, 1, SHRINK>(r);
+    if (nsites == 2) return vec ? pick_split_rank<T, true, 2, SHRINK>(r) : pick_split_rank<T, false, 2, SHRINK>(r);
+    return vec ? pick_split_rank<T, true, 3, SHRINK>(r) : pick_split_rank<T, false, 3, SHRINK>(r);
+}
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// -1 automatic, 0 SIMT only, 1 tensor cores only (env PREFT_SPLIT_VARIANT=simt|tc)
+static int g_split_variant = -2;
+int split_variant() {
+    if (g_split_variant == -2) {
+        const char* env = getenv("PREFT_SPLIT_VARIANT");
+        g_split_variant = (env && env[0] == 's') ? 0 : (env && env[0] == 't') ? 1 : -1;
+    }
+    return g_split_variant;
+}
+void set_split_variant(int v) { g_split_variant = v; }
+
+template <typename K>
+static int launch_tc(K kernel, int smem, int threads, const SplitMaps& maps, const SplitArgs& args, int num_sms,
+                     cudaStream_t stream) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return -static_cast<int>(e);
+    kernel<<<num_sms, threads, smem, stream>>>(maps, args);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? PREFT_OK : -static_cast<int>(e);
+}
+
+static int fill_common(SplitArgs& args, const preft_meta_t* meta, const preft_lora_site_t* sites, int nsites,
+                       void* P, long long ldp) {
+    args.nsites = nsites;
+    for (int s = 0; s < nsites; ++s) {
+        args.site[s].A = sites[s].A;
+        args.site[s].Bt = sites[s].Bt;
+        args.site[s].Bt_tc = sites[s].Bt_tc;
+        args.site[s].scale = sites[s].scale;
+        args.site[s].y = sites[s].y;
+        args.site[s].ldy = sites[s].ldy;
+        args.site[s].n = sites[s].n;
+    }
+    args.P = P;
+    args.ldp = ldp;
+    args.slot_base = meta->slot_split;
+    args.tokens = reinterpret_cast<const int2*>(meta->tokens);
+    args.chunks = reinterpret_cast<const int2*>(meta->chunks);
+    args.units = reinterpret_cast<const int4*>(meta->units);
+    args.counters = meta->counters;
+    return PREFT_OK;
+}
+
+int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
+                const preft_lora_site_t* sites, int nsites, int r, int dtype, void* P, long long ldp,
+                cudaStream_t stream, int num_sms) {
+    if (!meta || !x || !sites || !P || nsites < 1 || nsites > 3 || m < 1 || ldx < m || rows < 1) return PREFT_ERR_SHAPE;
+    if (r < 1 || r > 64 || (r & (r - 1)) || nsites * r > 64) return PREFT_ERR_RANK;
+    if (ldp < static_cast<long long>(nsites) * r) return PREFT_ERR_SHAPE;
+    if (dtype != PREFT_DTYPE_F32 && dtype != PREFT_DTYPE_BF16 && dtype != PREFT_DTYPE_F64) return PREFT_ERR_DOMAIN;
+    for (int s = 0; s < nsites; ++s)
+        if (!sites[s].A) return PREFT_ERR_SHAPE;
+    SplitArgs args{};
+    args.x = x;
+    args.ldx = ldx;
+    args.m = m;
+    fill_common(args, meta, sites, nsites, P, ldp);
+    const int variant = split_variant();
+    bool tc_ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && m % 64 == 0 && ldx % 8 == 0 && ldp % 4 == 0 &&
+                 al16(x) && al16(P) && meta->chunks && meta->units;
+    for (int s = 0; s < nsites; ++s) tc_ok = tc_ok && al16(sites[s].A);
+    if (variant == 1 && !tc_ok) return PREFT_ERR_SHAPE;
+    if (variant != 0 && tc_ok) {
+        SplitMaps maps{};
+        if (!make_tmap_bf16_sw128(&maps.x, x, static_cast<unsigned long long>(rows), static_cast<unsigned long long>(m),
+                                  static_cast<unsigned long long>(ldx), 64, kSpChunk))
+            return PREFT_ERR_CONFIG;
+        for (int s = 0; s < nsites; ++s)
+            if (!make_tmap_bf16_sw128(&maps.A[s], sites[s].A, 1ull << 20, static_cast<unsigned long long>(m),
+                                      static_cast<unsigned long long>(m), 64, static_cast<unsigned>(r)))
+                return PREFT_ERR_CONFIG;
+        if (r == 16) {
+            if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, 192, maps, args, num_sms, stream);
+            if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, 192, maps, args, num_sms, stream);
+            return launch_tc(shrink_tc_kernel<16, 3>, ShrinkLayout<16, 3>::SMEM, 192, maps, args, num_sms, stream);
+        }
+        if (nsites == 1) return launch_tc(shrink_tc_kernel<32, 1>, ShrinkLayout<32, 1>::SMEM, 192, maps, args, num_sms, stream);
+        if (nsites == 2) return launch_tc(shrink_tc_kernel<32, 2>, ShrinkLayout<32, 2>::SMEM, 192, maps, args, num_sms, stream);
+        return PREFT_ERR_RANK;  // 3 x 32 > 64 columns of P per row (checked above)
+    }
+    const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;
+    bool vec = m % W == 0 && ldx % W == 0 && al16(x);
+    for (int s = 0; s < nsites; ++s) vec = vec && al16(sites[s].A);
+    SplitFn fn = dtype == PREFT_DTYPE_BF16  ? pick_split<__nv_bfloat16, true>(vec, nsites, r)
+                 : dtype == PREFT_DTYPE_F32 ? pick_split<float, true>(vec, nsites, r)
+                                            : pick_split<double, true>(vec, nsites, r);
+    if (!fn) return PREFT_ERR_RANK;
+    fn<<<grid_for(reinterpret_cast<const void*>(fn), 256, num_sms), 256, 0, stream>>>(args);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PREFT_OK : -static_cast<int>(e);
+}
+
+int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long long rows, const preft_lora_site_t* sites,
+                int nsites, int r, int dtype, cudaStream_t stream, int num_sms) {
+    if (!meta || !P || !sites || nsites < 1 || nsites > 3 || rows < 1) return PREFT_ERR_SHAPE;
+    if (r < 1 || r > 64 || (r & (r - 1)) || nsites * r > 64) return PREFT_ERR_RANK;
+    if (ldp < static_cast<long long>(nsites) * r) return PREFT_ERR_SHAPE;
+    if (dtype != PREFT_DTYPE_F32 && dtype != PREFT_DTYPE_BF16 && dtype != PREFT_DTYPE_F64) return PREFT_ERR_DOMAIN;
+    for (int s = 0; s < nsites; ++s)
+        if (!sites[s].scale || !sites[s].y || sites[s].n < 1 || sites[s].ldy < sites[s].n) return PREFT_ERR_SHAPE;
+    SplitArgs args{};
+    fill_common(args, meta, sites, nsites, const_cast<void*>(P), ldp);
+    const int variant = split_variant();
+    bool tc_ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && ldp % 4 == 0 && al16(P) && meta->chunks &&
+                 meta->units;
+    for (int s = 0; s < nsites; ++s)
+        tc_ok = tc_ok && sites[s].Bt_tc && sites[s].n % kSpN == 0 && sites[s].ldy % 8 == 0 && al16(sites[s].y) &&
+                al16(sites[s].Bt_tc);
+    if (variant == 1 && !tc_ok) return PREFT_ERR_SHAPE;
+    if (variant != 0 && tc_ok) {
+        SplitMaps maps{};
+        for (int s = 0; s < nsites; ++s)
+            if (!make_tmap_bf16_sw128(&maps.y[s], sites[s].y, static_cast<unsigned long long>(rows),
+                                      static_cast<unsigned long long>(sites[s].n),
+                                      static_cast<unsigned long long>(sites[s].ldy), 64, kSpChunk))
+                return PREFT_ERR_CONFIG;
+        if (r == 16) {
+            if (nsites == 1) return launch_tc(expand_tc_kernel<16, 1>, ExpandLayout<16, 1>::SMEM, 384, maps, args, num_sms, stream);
+            if (nsites == 2) return launch_tc(expand_tc_kernel<16, 2>, ExpandLayout<16, 2>::SMEM, 384, maps, args, num_sms, stream);
+            return launch_tc(expand_tc_kernel<16, 3>, ExpandLayout<16, 3>::SMEM, 384, maps, args, num_sms, stream);
+        }
+        if (nsites == 1) return launch_tc(expand_tc_kernel<32, 1>, ExpandLayout<32, 1>::SMEM, 384, maps, args, num_sms, stream);
+        if (nsites == 2) return launch_tc(expand_tc_kernel<32, 2>, ExpandLayout<32, 2>::SMEM, 384, maps, args, num_sms, stream);
+        return PREFT_ERR_RANK;
+    }
+    const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;
+    bool vec = true;
+    for (int s = 0; s < nsites; ++s) {
+        if (!sites[s].Bt) return PREFT_ERR_SHAPE;  // the SIMT expand reads the row-major Bt
+        vec = vec && sites[s].n % W == 0 && sites[s].ldy % W == 0 && al16(sites[s].y) && al16(sites[s].Bt);
+    }
+    SplitFn fn = dtype == PREFT_DTYPE_BF16  ? pick_split<__nv_bfloat16, false>(vec, nsites, r)
+                 : dtype == PREFT_DTYPE_F32 ? pick_split<float, false>(vec, nsites, r)
+                                            : pick_split<double, false>(vec, nsites, r);
+    if (!fn) return PREFT_ERR_RANK;
+    fn<<<grid_for(reinterpret_cast<const void*>(fn), 256, num_sms), 256, 0, stream>>>(args);
+    const cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? PREFT_OK : -static_cast<int>(e);
+}
+
+}  // namespace preft

@@ -26,7 +26,7 @@ import torch
 
 from . import _lib
 from .adapters import AdapterKind, AdapterParams
-from .errors import ShapeError
+from .errors import ConfigError, ShapeError
 from .meta import BatchMeta, default_meta
 from .pool import AdapterPool, _round_rank, acc_dtype, torch_dtype_code
 
@@ -85,6 +85,8 @@ def apply_lora_group_(
         raise ShapeError(f"layer {layer} out of range")
     if not pool.lora_capacity:
         raise ShapeError("the pool holds no LoRA adapters")
+    if pool.tp_size > 1:
+        raise ConfigError("a tensor-parallel pool shard needs tp.apply_lora_group_tp_ (shrink, all-reduce, expand)")
     ms = {pool.lora_sites[s][1] for s in sites}
     if len(ms) != 1:
         raise ShapeError(f"sites {tuple(sites)} do not share an input width")

@@ -106,7 +106,11 @@ class AdapterPool:
         reft_rank: int = 16,
         dtype: torch.dtype = torch.bfloat16,
         device=None,
+        tp_rank: int = 0,
+        tp_size: int = 1,
     ):
+        from .tp import site_shard
+
         if n_layers < 1 or d_model < 1:
             raise ConfigError("n_layers and d_model must be >= 1")
         if lora_capacity < 0 or reft_capacity < 0 or lora_capacity + reft_capacity < 1:
@@ -135,12 +139,23 @@ class AdapterPool:
         self.reft_tc = False
         self.lora_A: dict[str, torch.Tensor] = {}
         self.lora_Bt: dict[str, torch.Tensor] = {}
+        self.lora_Bt_tc: dict[str, torch.Tensor] = {}
         self.lora_scale: dict[str, torch.Tensor] = {}
-        for name, (n, m) in self.lora_sites.items():
+        # tensor parallelism (tp.py): every LoRA site keeps A sharded along its
+        # input dim and B along its output dim; tp_size == 1 is the whole site
+        self.tp_rank, self.tp_size = int(tp_rank), int(tp_size)
+        self.lora_shard = {name: site_shard(name, n, m, self.tp_rank, self.tp_size)
+                           for name, (n, m) in self.lora_sites.items()}
+        lora_tc = dtype == torch.bfloat16 and self.lora_rank in (16, 32)
+        for name, sh in self.lora_shard.items():
             if self.lora_capacity:
-                self.lora_A[name] = torch.zeros(L, self.lora_capacity, self.lora_rank, m, **z)
-                self.lora_Bt[name] = torch.zeros(L, self.lora_capacity, self.lora_rank, n, **z)
+                self.lora_A[name] = torch.zeros(L, self.lora_capacity, self.lora_rank, sh.m_loc, **z)
+                self.lora_Bt[name] = torch.zeros(L, self.lora_capacity, self.lora_rank, sh.n_loc, **z)
                 self.lora_scale[name] = torch.zeros(L, self.lora_capacity, **za)
+                if lora_tc and sh.n_loc % 128 == 0:
+                    # B (= Bt^T) pre-tiled for the tensor-core expand (csrc/lora_split.cu)
+                    self.lora_Bt_tc[name] = torch.zeros(L, self.lora_capacity, sh.n_loc // 8, self.lora_rank // 8,
+                                                        8, 8, **z)
         if self.reft_capacity:
             S, R, d = self.reft_capacity, self.reft_rank, self.d_model
             self.reft_A = torch.zeros(L, S, R, d, **z)
@@ -174,7 +189,8 @@ class AdapterPool:
 
     @property
     def nbytes(self) -> int:
-        tensors: list[torch.Tensor] = [*self.lora_A.values(), *self.lora_Bt.values(), *self.lora_scale.values()]
+        tensors: list[torch.Tensor] = [*self.lora_A.values(), *self.lora_Bt.values(), *self.lora_scale.values(),
+                                       *self.lora_Bt_tc.values()]
         if self.reft_capacity:
             tensors += [self.reft_A, self.reft_B, self.reft_bias, self.reft_scale]
             if self.reft_Bt is not None:
@@ -303,11 +319,15 @@ class AdapterPool:
                 self.lora_scale[name][:, slot].zero_()
             scales: dict[str, np.ndarray] = {name: np.zeros(self.n_layers) for name in self.lora_sites}
             for (layer, name), p in adapter.lora_sites.items():
-                n, m = p.dims
+                sh = self.lora_shard[name]
                 r = p.rank
-                plan.append((self.lora_A[name][layer, slot], self.dtype_code, add(p.A), m, 1, r, R, m))
+                m, n = sh.m_loc, sh.n_loc
+                # this rank's slice: A columns [m0, m0+m_loc), B rows [n0, n0+n_loc)
+                A = np.asarray(p.A)[:, sh.m0 : sh.m0 + m]
+                B = np.asarray(p.B)[sh.n0 : sh.n0 + n, :]
+                plan.append((self.lora_A[name][layer, slot], self.dtype_code, add(A), m, 1, r, R, m))
                 # B is (n, r) row-major: Bt[k][j] = B[j][k] -> src strides (1, r)
-                plan.append((self.lora_Bt[name][layer, slot], self.dtype_code, add(p.B), 1, r, r, R, n))
+                plan.append((self.lora_Bt[name][layer, slot], self.dtype_code, add(B), 1, r, r, R, n))
                 scales[name][layer] = p.prefactor
             for name, sc in scales.items():
                 plan.append((self.lora_scale[name][:, slot].unsqueeze(1), acc_code, add(sc), 1, 1, self.n_layers,
@@ -331,6 +351,9 @@ class AdapterPool:
         dev = host.to(self.device, non_blocking=False)
         for dst, code, o, srow, scol, rv, rows, cols in plan:
             self._convert(dst, code, dev, o, srow, scol, rv, rows, cols, s)
+        if adapter.kind is AdapterKind.LORA:
+            for name, tc in self.lora_Bt_tc.items():
+                tc[:, slot].copy_(tile_kmajor(self.lora_Bt[name][:, slot].transpose(-1, -2)))
         if adapter.kind is not AdapterKind.LORA and self.reft_Bt is not None:
             # the tensor-core copy is a pure permutation of the converted B slab
             j = slot - self.slot_split
@@ -343,6 +366,8 @@ class AdapterPool:
                 self.lora_A[name][:, info.slot].zero_()
                 self.lora_Bt[name][:, info.slot].zero_()
                 self.lora_scale[name][:, info.slot].zero_()
+                if name in self.lora_Bt_tc:
+                    self.lora_Bt_tc[name][:, info.slot].zero_()
         else:
             j = info.slot - self.slot_split
             self.reft_A[:, j].zero_()
@@ -391,12 +416,16 @@ class AdapterPool:
             if rank > self.lora_rank:
                 raise RankError(f"rank {rank} exceeds the pool's LoRA rank {self.lora_rank}")
             slots = torch.tensor([self._slots[a].slot for a in ids], device=self.device)
-            for name, (n, m) in self.lora_sites.items():
+            for name, sh in self.lora_shard.items():
+                n, m = sh.n_loc, sh.m_loc
                 for layer in range(self.n_layers):
                     A = torch.randn(len(ids), rank, m, generator=g, device=self.device, dtype=torch.float32) * sigma
                     Bt = torch.randn(len(ids), rank, n, generator=g, device=self.device, dtype=torch.float32) * sigma
                     self.lora_A[name][layer].index_copy_(0, slots, torch.nn.functional.pad(A, (0, 0, 0, self.lora_rank - rank)).to(self.dtype))
-                    self.lora_Bt[name][layer].index_copy_(0, slots, torch.nn.functional.pad(Bt, (0, 0, 0, self.lora_rank - rank)).to(self.dtype))
+                    Btp = torch.nn.functional.pad(Bt, (0, 0, 0, self.lora_rank - rank)).to(self.dtype)
+                    self.lora_Bt[name][layer].index_copy_(0, slots, Btp)
+                    if name in self.lora_Bt_tc:
+                        self.lora_Bt_tc[name][layer].index_copy_(0, slots, tile_kmajor(Btp.transpose(1, 2)))
                 self.lora_scale[name].index_fill_(1, slots, 32.0 / rank)
         else:
             if rank > self.reft_rank:
