@@ -512,6 +512,107 @@ def lora_reft_mix_config(args, device) -> dict:
             "value": round(4096 / (ms / 1e3), 1), "unit": "tokens/s per (layer, site pair)"}
 
 
+def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | None:
+    """BASELINE config 4: Llama-3.1-70B shapes (80 layers, 7 LoRA^P sites), 512
+    LoRA^P r=16 adapters, 8-way tensor parallelism with the pool sharded along
+    m (A) and n (B) and the rank-r shrink partials all-reduced over NCCL
+    (tp.py).  At 8 GPUs the real TP group runs; on 1 GPU rank 0's share of the
+    work runs without the collective (its 26.5 GB shard of the pool, the same
+    batch).  Each step is CUDA-graph replayed (shrink, all-reduce, expand per
+    group and layer)."""
+    import torch
+
+    from paper_2605_14217_b200 import AdapterKind, shapes
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.pool import AdapterPool
+    from paper_2605_14217_b200.tp import SplitWorkspace, apply_lora_group_tp_
+
+    tp = 8
+    if world not in (1, tp):
+        return None
+    real = world == tp
+    shape = shapes.LLAMA_70B
+    r = 16
+    dims = shape.site_dims()
+    pool = AdapterPool(shape.n_layers, shape.d_model, lora_sites=dims, lora_capacity=N_ADAPTERS, lora_rank=r,
+                       dtype=torch.bfloat16, device=device, tp_rank=rank if real else 0, tp_size=tp)
+    pool.fill_synthetic_(N_ADAPTERS, AdapterKind.LORA, r, seed=23, sigma=0.01)
+    qsl, ids, flags, lens, _ = step_entries(0, 1, args.requests, args.decodes, seed=SEED + 3)
+    slots = pool.entry_arrays(qsl, ids, flags)
+    T = int(qsl[-1])
+    meta = BatchMeta(len(ids), T, tile_tokens=128, device=device)
+    meta.set_slot_split(pool.slot_split)
+    meta.build_arrays(qsl, slots, flags)
+    ws = SplitWorkspace(meta, pool)
+    g = torch.Generator(device=device)
+    g.manual_seed(77 + rank)
+    sets = []
+    for _ in range(2):  # two activation sets alternate across layers (> L2 between reuses)
+        acts = {}
+        for group in shapes.SITE_GROUPS:
+            sh = pool.lora_shard[group[0]]
+            x = torch.randn(T, sh.x_width, generator=g, device=device).to(torch.bfloat16)
+            ys = [torch.randn(T, pool.lora_shard[s].y_width, generator=g, device=device).to(torch.bfloat16)
+                  for s in group]
+            acts[group] = (x, ys)
+        sets.append(acts)
+
+    def step(s):
+        for layer in range(shape.n_layers):
+            acts = sets[layer % 2]
+            for group in shapes.SITE_GROUPS:
+                x, ys = acts[group]
+                apply_lora_group_tp_(ys, x, meta, pool, layer, group, workspace=ws, stream=s, collective=real)
+
+    s = torch.cuda.current_stream(device)
+    for _ in range(2):
+        step(s)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream(device)
+    cs.wait_stream(s)
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(graph, stream=cs):
+            step(cs)
+    s.wait_stream(cs)
+    for _ in range(2):
+        graph.replay()
+    torch.cuda.synchronize()
+    barrier(world)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    for _ in range(steps):
+        graph.replay()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = all_max(e0.elapsed_time(e1) / steps, world)
+    sel = int(lens.sum())
+    distinct = len({ids[i] for i in range(len(ids)) if not (flags[i] & 1)})
+    # algorithmic bytes per rank per step (SURVEY 8(d), sharded): x slice read,
+    # y slice read + written, each distinct adapter's A / B shard once, P
+    # written by the shrink and read by the expand (f32)
+    per_layer = 0
+    for group in shapes.SITE_GROUPS:
+        m_loc = pool.lora_shard[group[0]].m_loc
+        n_locs = [pool.lora_shard[t].n_loc for t in group]
+        per_layer += sel * 2 * (m_loc + 2 * sum(n_locs)) + distinct * 2 * r * sum(m_loc + n for n in n_locs)
+        per_layer += 2 * sel * 4 * r * len(group)
+    step_bytes = shape.n_layers * per_layer
+    peak, _ = measured_peak_gbs()
+    frac = step_bytes / (ms / 1e3) / 1e9 / peak
+    allreduce_bytes = shape.n_layers * sum(T * 4 * r * len(gp) for gp in shapes.SITE_GROUPS)
+    out = {"workload": "cfg4: Llama-3.1-70B shapes, 80 layers x 7 LoRA^P sites, 512 LoRA^P r16, TP=8 "
+                       + ("(8 GPUs, NCCL all-reduce of the rank-r partials)" if real else
+                          "(1 GPU: rank 0's shard and work, all-reduce omitted)"),
+           "prefill_tokens": sel, "ms_per_step": round(ms, 3), "value": round(sel / (ms / 1e3), 1), "unit": UNIT,
+           "per_rank_frac_of_hbm_peak": round(frac, 4), "per_rank_algorithmic_bytes": int(step_bytes),
+           "allreduce_bytes_per_rank_per_step": int(allreduce_bytes) if real else 0,
+           "pool_gb_per_rank": round(pool.nbytes / 1e9, 2), "launch": "cuda graph"}
+    del pool, meta, ws, sets, graph
+    torch.cuda.empty_cache()
+    return out
+
+
 def secondary_configs(args, device) -> list:
     from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig, assign_adapters
 
@@ -581,10 +682,13 @@ def run_ours(args):
     if not args.no_punica_step and world == 1:
         punica = punica_step(args, rank, world, device)
     others = None
-    if not args.no_secondary and world == 1:
+    if not args.no_secondary and world in (1, 8):
         del ctx["plan"], ctx["acts"]
         torch.cuda.empty_cache()
-        others = secondary_configs(args, device)
+        others = secondary_configs(args, device) if world == 1 else []
+        cfg4 = tp_config(args, device, world, rank)
+        if cfg4 is not None:
+            others.append(cfg4)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(ctx, args.cpu_seconds)

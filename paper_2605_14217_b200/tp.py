@@ -209,13 +209,16 @@ def apply_lora_group_tp_(
     group=None,
     workspace: SplitWorkspace | None = None,
     stream=None,
+    collective: bool = True,
 ):
     """Tensor-parallel y_s[rows] += s_a (x[rows] A_s,a^T) B_s,a^T for 1-3 sites
     sharing x, on this rank's shard of the pool (`pool.tp_rank` of
     `pool.tp_size`): shrink, NCCL all-reduce of the rank-r partials on the
     same stream, expand.  `x` and `ys` follow the site's TP style (see the
     module docstring); `group` is the torch.distributed process group of the
-    TP ranks (None = default group; no collective when tp_size == 1)."""
+    TP ranks (None = default group; no collective when tp_size == 1).
+    collective=False skips the all-reduce (single-GPU emulation of one rank's
+    share of the work; the result is then this rank's partial only)."""
     import torch
 
     ws = workspace if workspace is not None else SplitWorkspace(meta, pool)
@@ -223,10 +226,10 @@ def apply_lora_group_tp_(
     per = max(1, 64 // pool.lora_rank)  # a launch carries <= 64 rank-r columns of P
     if len(sites) > per:
         for i in range(0, len(sites), per):
-            apply_lora_group_tp_(ys[i : i + per], x, meta, pool, layer, sites[i : i + per], group, ws, s)
+            apply_lora_group_tp_(ys[i : i + per], x, meta, pool, layer, sites[i : i + per], group, ws, s, collective)
         return ys
     P = lora_shrink_tp_(ys, x, meta, pool, layer, sites, ws, s)
-    if pool.tp_size > 1:
+    if pool.tp_size > 1 and collective:
         import torch.distributed as dist
 
         with torch.cuda.stream(s):
