@@ -217,6 +217,9 @@ int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int6
 /* split-kernel variant: -1 automatic, 0 SIMT only, 1 tensor cores only
  * (PREFT_ERR_SHAPE when ineligible).  Env: PREFT_SPLIT_VARIANT=simt|tc. */
 int preft_set_split_variant(int32_t variant);
+/* Diagnostic: clock64() stamps of the tensor-core shrink's CTA 0 (4 per
+ * panel / unit, 512 int64, NULL = off). */
+int preft_diag_split(long long* device_buffer);
 
 /*
  * K3 (h has `rows` allocated rows; TMA bounds): h[t,:] += s_a * ((h[t,:] . A_a^T + b_a) . B_a)   for every selected token

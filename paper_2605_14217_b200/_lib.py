@@ -153,6 +153,7 @@ SIGNATURES = {
         ],
     ),
     "preft_set_split_variant": (ctypes.c_int, [ctypes.c_int32]),
+    "preft_diag_split": (ctypes.c_int, [ctypes.c_void_p]),
     "preft_diag_reft_tc": (ctypes.c_int, [ctypes.c_void_p]),
     "preft_convert_2d": (
         ctypes.c_int,

@@ -16,6 +16,7 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
                int num_sms);
 void set_reft_variant(int v);
 void set_split_variant(int v);
+void split_set_profile(long long* buf);
 int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
                 const preft_lora_site_t* sites, int nsites, int r, int dtype, void* P, long long ldp,
                 cudaStream_t stream, int num_sms);
@@ -182,6 +183,11 @@ int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int6
                       const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype, void* stream) {
     return finish(lora_expand(meta, P, ldp, rows, sites, nsites, r_max, dtype, static_cast<cudaStream_t>(stream),
                               current_num_sms()));
+}
+
+int preft_diag_split(long long* device_buffer) {
+    split_set_profile(device_buffer);
+    return PREFT_OK;
 }
 
 int preft_set_split_variant(int32_t variant) {

@@ -50,7 +50,8 @@ struct SplitArgs {
     void* P;  // [rows][ldp] acc type
     long long ldp;
     int slot_base;  // LoRA-class slots are < slot_base (meta->slot_split)
-    int pad;
+    int ks;         // tensor-core shrink: K splits per unit (1 or 2)
+    long long* prof;  // diagnostics: clock64 stamps of CTA 0 (NULL in production)
     const int2* tokens;
     const int2* chunks;
     const int4* units;
@@ -196,9 +197,9 @@ struct ShrinkLayout {
     static constexpr int TMEM_COLS = 2 * kSpAcc * NSR <= 256 ? 256 : 512;
 };
 
-// warps: 0 TMA producer, 1 UMMA issuer, 2..5 TMEM -> P rows (lane quadrant = warp % 4)
+// warps: 0 TMA producer (x), 6 TMA producer (A), 1 UMMA issuer, 2..5 TMEM -> P rows (lane quadrant = warp % 4)
 template <int R, int NS>
-__global__ void __launch_bounds__(192, 1) shrink_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
+__global__ void __launch_bounds__(224, 1) shrink_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
     using L = ShrinkLayout<R, NS>;
     extern __shared__ unsigned char sm_raw[];
     __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
@@ -223,30 +224,56 @@ __global__ void __launch_bounds__(192, 1) shrink_tc_kernel(const __grid_constant
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tslot;
-    int u0, u1;
-    even_share(a.counters[PREFT_CTR_UNITS], blockIdx.x, gridDim.x, u0, u1);
+    // work item = (unit, 1/ks of the K panels): ks = 2 balances launches with
+    // ~2 units per SM; the two halves meet in P through f32 atomics, whose
+    // order cannot change a two-term sum (0 + a + b == 0 + b + a)
+    const int ks = a.ks;
+    int w0, w1;
+    even_share(a.counters[PREFT_CTR_UNITS] * ks, blockIdx.x, gridDim.x, w0, w1);
     const int NP = a.m / 64;
 
     if (warp == 0) {
+        // x producer: lane q issues chunk q's box, so a stage's boxes are in
+        // flight together (one thread pays ~100+ cycles per TMA issue)
+        const uint64_t stream = tc::policy_evict_first();
+        int stage = 0, npf = 0;
+        uint32_t phase = 0;
+        for (int w = w0; w < w1; ++w) {
+            const int4 U = a.units[w / ks];
+            if (U.x >= a.slot_base) continue;  // ReFT-class unit
+            const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
+            const int nch = U.z;
+            const int row = lane < nch ? a.chunks[U.y + lane].x : 0;
+            const uint32_t bytes = static_cast<uint32_t>(nch * kSpChunk * 128 + NS * L::AP_BYTES);
+            for (int p = p0; p < p1; ++p) {
+                if (lane == 0) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1u);
+                    if (a.prof && blockIdx.x == 0 && npf < 128) a.prof[npf * 4 + 0] = clock64();
+                    tc::mbar_expect_tx(&full[stage], bytes);
+                }
+                __syncwarp();
+                const uint32_t st = sbase + stage * L::STAGE;
+                if (lane < nch) tc::tma_load_2d_hint(st + lane * (kSpChunk * 128), &maps.x, p * 64, row, &full[stage], stream);
+                ++npf;
+                if (++stage == L::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+    } else if (warp == 6) {
+        // second producer: the adapters' A panels (TMA issue costs ~100+ cycles
+        // per box from one thread, so x and A boxes are issued from two warps)
         if (lane == 0) {
-            const uint64_t stream = tc::policy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = u0; u < u1; ++u) {
-                const int4 U = a.units[u];
-                if (U.x >= a.slot_base) continue;  // ReFT-class unit
-                const int nch = U.z;
-                int rows[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
-                const uint32_t bytes = static_cast<uint32_t>(nch * kSpChunk * 128 + NS * L::AP_BYTES);
-                for (int p = 0; p < NP; ++p) {
+            for (int w = w0; w < w1; ++w) {
+                const int4 U = a.units[w / ks];
+                if (U.x >= a.slot_base) continue;
+                const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
+                for (int p = p0; p < p1; ++p) {
                     tc::mbar_wait(&empty[stage], phase ^ 1u);
                     const uint32_t st = sbase + stage * L::STAGE;
-                    tc::mbar_expect_tx(&full[stage], bytes);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (q < nch) tc::tma_load_2d_hint(st + q * (kSpChunk * 128), &maps.x, p * 64, rows[q], &full[stage], stream);
 #pragma unroll
                     for (int s = 0; s < NS; ++s)
                         tc::tma_load_2d(st + L::X_BYTES + s * L::AP_BYTES, &maps.A[s], p * 64, U.x * R, &full[stage]);
@@ -259,29 +286,30 @@ __global__ void __launch_bounds__(192, 1) shrink_tc_kernel(const __grid_constant
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t id = tc::idesc_bf16_f32(kSpU, R);
-            int stage = 0, ub = 0;
+            // the sites' A panels sit back to back in the stage, so one UMMA with
+            // N = NS * R covers all of them (tiny-N UMMAs cost ~60-90 cycles each)
+            const uint32_t id = tc::idesc_bf16_f32(kSpU, L::NSR);
+            int stage = 0, ub = 0, nmc = 0;
             uint32_t phase = 0;
-            for (int u = u0; u < u1; ++u) {
-                const int4 U = a.units[u];
+            for (int w = w0; w < w1; ++w) {
+                const int4 U = a.units[w / ks];
                 if (U.x >= a.slot_base) continue;
+                const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
                 const int sb = ub & 1;
                 tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
                 tc::fence_after_sync();
                 const uint32_t dS = tmem + sb * kSpAcc * L::NSR;
-                for (int p = 0; p < NP; ++p) {
+                for (int p = p0; p < p1; ++p) {
                     tc::mbar_wait(&full[stage], phase);
+                    if (a.prof && blockIdx.x == 0 && nmc < 128) a.prof[nmc * 4 + 1] = clock64();
+                    ++nmc;
                     tc::fence_after_sync();
                     const uint32_t st = sbase + stage * L::STAGE;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        const int kk = p * 4 + k;
-                        const uint64_t ad = tc::desc_kmajor_sw128(st + k * 32);
-#pragma unroll
-                        for (int s = 0; s < NS; ++s)
-                            tc::mma_bf16(dS + (kk % kSpAcc) * L::NSR + s * R, ad,
-                                         tc::desc_kmajor_sw128(st + L::X_BYTES + s * L::AP_BYTES + k * 32), id,
-                                         kk >= kSpAcc ? 1u : 0u);
+                        const int kk = (p - p0) * 4 + k;
+                        tc::mma_bf16(dS + (kk % kSpAcc) * L::NSR, tc::desc_kmajor_sw128(st + k * 32),
+                                     tc::desc_kmajor_sw128(st + L::X_BYTES + k * 32), id, kk >= kSpAcc ? 1u : 0u);
                     }
                     tc::mma_commit(&empty[stage]);
                     if (++stage == L::STAGES) {
@@ -293,16 +321,17 @@ __global__ void __launch_bounds__(192, 1) shrink_tc_kernel(const __grid_constant
                 ++ub;
             }
         }
-    } else {
+    } else if (warp < 6) {
         const int q = warp & 3;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int ub = 0;
-        for (int u = u0; u < u1; ++u) {
-            const int4 U = a.units[u];
+        for (int w = w0; w < w1; ++w) {
+            const int4 U = a.units[w / ks];
             if (U.x >= a.slot_base) continue;
             const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
             const int sb = ub & 1;
             tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
+            if (a.prof && blockIdx.x == 0 && lane == 0 && q == 0 && ub < 128) a.prof[ub * 4 + 2] = clock64();
             tc::fence_after_sync();
             float s[L::NSR];
 #pragma unroll
@@ -322,9 +351,14 @@ __global__ void __launch_bounds__(192, 1) shrink_tc_kernel(const __grid_constant
             if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
             if (lane < ch.y) {
                 float* pr = static_cast<float*>(a.P) + static_cast<long long>(ch.x + lane) * a.ldp;
+                if (ks == 1) {
 #pragma unroll
-                for (int c = 0; c < L::NSR; c += 4)
-                    *reinterpret_cast<float4*>(pr + c) = make_float4(s[c], s[c + 1], s[c + 2], s[c + 3]);
+                    for (int c = 0; c < L::NSR; c += 4)
+                        *reinterpret_cast<float4*>(pr + c) = make_float4(s[c], s[c + 1], s[c + 2], s[c + 3]);
+                } else {
+#pragma unroll
+                    for (int c = 0; c < L::NSR; ++c) atomicAdd(pr + c, s[c]);
+                }
             }
             ++ub;
         }
@@ -348,6 +382,34 @@ struct ExpandLayout {
     static constexpr int STAGES_FIT = (227 * 1024 - 2048 - OFF_RING) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int SMEM = OFF_RING + STAGES * STAGE + 1024;
+};
+
+// The expand's work item is (unit, block of kExpBlock 128-column chunks) over
+// the concatenated chunks of all sites, so a launch balances across CTAs even
+// when a batch has few units per SM (Punica-sized steps: ~2 units per CTA,
+// but 56 gate/up chunks per unit).  Consecutive items of one unit share its V.
+constexpr int kExpBlock = 4;
+
+struct ExpandItems {
+    int w0, w1;  // this CTA's contiguous share of items
+    int ipu;     // items per unit
+    int nc;      // chunks per unit (all sites)
+    int off[4];  // first chunk of each site
+    __device__ void init(const SplitArgs& a, int nsites) {
+        nc = 0;
+        for (int s = 0; s < nsites; ++s) {
+            off[s] = nc;
+            nc += a.site[s].n / kSpN;
+        }
+        off[nsites] = nc;
+        ipu = (nc + kExpBlock - 1) / kExpBlock;
+        even_share(a.counters[PREFT_CTR_UNITS] * ipu, blockIdx.x, gridDim.x, w0, w1);
+    }
+    __device__ void site_of(int c, int nsites, int& s, int& j) const {
+        s = 0;
+        while (s + 1 < nsites && c >= off[s + 1]) ++s;
+        j = c - off[s];
+    }
 };
 
 // warps: 0 TMA producer, 1 UMMA issuer, 2-3 P rows -> bf16 hi/lo V, 4-11 epilogue
@@ -380,44 +442,43 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tslot;
-    int u0, u1;
-    even_share(a.counters[PREFT_CTR_UNITS], blockIdx.x, gridDim.x, u0, u1);
+    ExpandItems it;
+    it.init(a, NS);
 
     if (warp == 0) {
         if (lane == 0) {
             const uint64_t stream = tc::policy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = u0; u < u1; ++u) {
-                const int4 U = a.units[u];
+            for (int w = it.w0; w < it.w1; ++w) {
+                const int4 U = a.units[w / it.ipu];
                 if (U.x >= a.slot_base) continue;
                 const int nch = U.z;
                 int rows[4];
 #pragma unroll
                 for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
                 const uint32_t bytes = static_cast<uint32_t>(2 * nch * kSpChunk * 128 + L::BT_BYTES);
-#pragma unroll 1
-                for (int s = 0; s < NS; ++s) {
-                    const int NJ = a.site[s].n / kSpN;
-                    const unsigned char* bt =
-                        static_cast<const unsigned char*>(a.site[s].Bt_tc) + static_cast<long long>(U.x) * a.site[s].n * R * 2;
-                    for (int j = 0; j < NJ; ++j) {
-                        tc::mbar_wait(&empty[stage], phase ^ 1u);
-                        const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
-                        tc::mbar_expect_tx(&full[stage], bytes);
+                const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
+                for (int c = c0; c < c1; ++c) {
+                    int s, j;
+                    it.site_of(c, NS, s, j);
+                    const unsigned char* bt = static_cast<const unsigned char*>(a.site[s].Bt_tc) +
+                                              static_cast<long long>(U.x) * a.site[s].n * R * 2;
+                    tc::mbar_wait(&empty[stage], phase ^ 1u);
+                    const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
+                    tc::mbar_expect_tx(&full[stage], bytes);
 #pragma unroll
-                        for (int pp = 0; pp < 2; ++pp)
+                    for (int pp = 0; pp < 2; ++pp)
 #pragma unroll
-                            for (int q = 0; q < 4; ++q)
-                                if (q < nch)
-                                    tc::tma_load_2d_hint(st + pp * kSpU * 128 + q * (kSpChunk * 128), &maps.y[s],
-                                                         j * kSpN + pp * 64, rows[q], &full[stage], stream);
-                        tc::bulk_load_1d(st + L::Y_BYTES, bt + static_cast<long long>(j) * L::BT_BYTES, L::BT_BYTES,
-                                         &full[stage]);
-                        if (++stage == L::STAGES) {
-                            stage = 0;
-                            phase ^= 1u;
-                        }
+                        for (int q = 0; q < 4; ++q)
+                            if (q < nch)
+                                tc::tma_load_2d_hint(st + pp * kSpU * 128 + q * (kSpChunk * 128), &maps.y[s],
+                                                     j * kSpN + pp * 64, rows[q], &full[stage], stream);
+                    tc::bulk_load_1d(st + L::Y_BYTES, bt + static_cast<long long>(j) * L::BT_BYTES, L::BT_BYTES,
+                                     &full[stage]);
+                    if (++stage == L::STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
                     }
                 }
             }
@@ -425,56 +486,67 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t id = tc::idesc_bf16_f32(kSpU, kSpN);
-            int stage = 0, ub = 0, dc = 0;
+            int stage = 0, visit = 0, dc = 0, prev = -1;
             uint32_t phase = 0;
-            for (int u = u0; u < u1; ++u) {
+            for (int w = it.w0; w < it.w1; ++w) {
+                const int u = w / it.ipu;
                 const int4 U = a.units[u];
                 if (U.x >= a.slot_base) continue;
-                const int vb = ub & 1;
-                tc::mbar_wait(&v_full[vb], (ub >> 1) & 1);
-                tc::fence_after_sync();
-#pragma unroll 1
-                for (int s = 0; s < NS; ++s) {
-                    const uint32_t vhi = sbase + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES, vlo = vhi + L::V_BYTES;
-                    const int NJ = a.site[s].n / kSpN;
-                    for (int j = 0; j < NJ; ++j) {
-                        tc::mbar_wait(&full[stage], phase);
-                        const int db = dc & 1;
-                        tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
-                        tc::fence_after_sync();
-                        const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
-                        const uint32_t dD = tmem + db * kSpN;
-#pragma unroll
-                        for (int k = 0; k < R / 16; ++k) {
-                            const uint64_t bd = tc::desc_kmajor(bt + k * 256, 128, R * 16);
-                            tc::mma_bf16(dD, tc::desc_kmajor(vhi + k * 256, 128, R * 16), bd, id, k > 0 ? 1u : 0u);
-                            tc::mma_bf16(dD, tc::desc_kmajor(vlo + k * 256, 128, R * 16), bd, id, 1u);
-                        }
-                        tc::mma_commit(&d_full[db]);
-                        tc::mma_commit(&empty[stage]);
-                        if (++stage == L::STAGES) {
-                            stage = 0;
-                            phase ^= 1u;
-                        }
-                        ++dc;
-                    }
+                const int vb = visit & 1;
+                if (u != prev) {
+                    tc::mbar_wait(&v_full[vb], (visit >> 1) & 1);
+                    tc::fence_after_sync();
+                    prev = u;
                 }
-                tc::mma_commit(&v_empty[vb]);
-                ++ub;
+                const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
+                for (int c = c0; c < c1; ++c) {
+                    int s, j;
+                    it.site_of(c, NS, s, j);
+                    const uint32_t vhi = sbase + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES, vlo = vhi + L::V_BYTES;
+                    tc::mbar_wait(&full[stage], phase);
+                    const int db = dc & 1;
+                    tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
+                    tc::fence_after_sync();
+                    const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
+                    const uint32_t dD = tmem + db * kSpN;
+#pragma unroll
+                    for (int k = 0; k < R / 16; ++k) {
+                        const uint64_t bd = tc::desc_kmajor(bt + k * 256, 128, R * 16);
+                        tc::mma_bf16(dD, tc::desc_kmajor(vhi + k * 256, 128, R * 16), bd, id, k > 0 ? 1u : 0u);
+                        tc::mma_bf16(dD, tc::desc_kmajor(vlo + k * 256, 128, R * 16), bd, id, 1u);
+                    }
+                    tc::mma_commit(&d_full[db]);
+                    tc::mma_commit(&empty[stage]);
+                    if (++stage == L::STAGES) {
+                        stage = 0;
+                        phase ^= 1u;
+                    }
+                    ++dc;
+                }
+                // the unit's V buffer is free once its last item has been issued
+                const bool last = w + 1 >= it.w1 || (w + 1) / it.ipu != u;
+                if (last) {
+                    tc::mma_commit(&v_empty[vb]);
+                    ++visit;
+                    prev = -1;
+                }
             }
         }
     } else if (warp < 4) {
-        // P rows -> V = scale * P (bf16 hi + lo), 32 rows per warp
-        int ub = 0;
-        for (int u = u0; u < u1; ++u) {
+        // P rows -> V = scale * P (bf16 hi + lo), 32 rows per warp, once per unit visit
+        int visit = 0, prev = -1;
+        for (int w = it.w0; w < it.w1; ++w) {
+            const int u = w / it.ipu;
             const int4 U = a.units[u];
             if (U.x >= a.slot_base) continue;
-            const int vb = ub & 1;
+            if (u == prev) continue;
+            prev = u;
+            const int vb = visit & 1;
             const int m = (warp - 2) * 32 + lane, q = m >> 4, rr = m & 15;
             const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
             const bool valid = rr < ch.y;
             const float* pr = static_cast<const float*>(a.P) + static_cast<long long>(ch.x + rr) * a.ldp;
-            tc::mbar_wait(&v_empty[vb], ((ub >> 1) & 1) ^ 1u);
+            tc::mbar_wait(&v_empty[vb], ((visit >> 1) & 1) ^ 1u);
 #pragma unroll
             for (int s = 0; s < NS; ++s) {
                 const float sc = __ldg(static_cast<const float*>(a.site[s].scale) + U.x);
@@ -504,7 +576,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
             tc::fence_proxy_async();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&v_full[vb]);
-            ++ub;
+            ++visit;
         }
     } else {
         // epilogue: D -> registers, y chunk += D in shared memory, TMA store
@@ -512,84 +584,89 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         const uint64_t stream = tc::policy_evict_first();
         const int r1 = lane >> 2, cp = 2 * (lane & 3);
-        int stage = 0, dc = 0;
+        int stage = 0, dc = 0, pend = -1;
         uint32_t phase = 0;
-        for (int u = u0; u < u1; ++u) {
-            const int4 U = a.units[u];
+        for (int w = it.w0; w < it.w1; ++w) {
+            const int4 U = a.units[w / it.ipu];
             if (U.x >= a.slot_base) continue;
             const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-#pragma unroll 1
-            for (int s = 0; s < NS; ++s) {
-                const int NJ = a.site[s].n / kSpN;
-                for (int j = 0; j < NJ; ++j) {
-                    const int db = dc & 1;
-                    tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
-                    tc::mbar_wait(&full[stage], phase);
-                    tc::fence_after_sync();
-                    uint32_t v[32];
-                    tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpN + hf * 64, v);
-                    tc::tmem_ld_wait();
-                    tc::fence_before_sync();
+            const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
+            for (int c = c0; c < c1; ++c) {
+                int s, j;
+                it.site_of(c, NS, s, j);
+                const int db = dc & 1;
+                tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
+                tc::mbar_wait(&full[stage], phase);
+                tc::fence_after_sync();
+                uint32_t v[32];
+                tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpN + hf * 64, v);
+                tc::tmem_ld_wait();
+                tc::fence_before_sync();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&d_empty[db]);
+                const uint32_t panel = L::OFF_RING + stage * L::STAGE + hf * kSpU * 128;
+                if (ch.y > 0) {
+                    uint32_t hv[16];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half)
+                            hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
+                                sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64));
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            float lo, hi;
+                            bf16x2_to_acc(hv[2 * i + half], lo, hi);
+                            lo += __uint_as_float(v[4 * i + 2 * half]);
+                            hi += __uint_as_float(v[4 * i + 2 * half + 1]);
+                            hv[2 * i + half] = f32x2_to_bf16(lo, hi);
+                        }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half)
+                            *reinterpret_cast<uint32_t*>(
+                                sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64)) =
+                                hv[2 * i + half];
+                    tc::fence_proxy_async();
                     __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&d_empty[db]);
-                    const uint32_t panel = L::OFF_RING + stage * L::STAGE + hf * kSpU * 128;
-                    if (ch.y > 0) {
-                        uint32_t hv[16];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half)
-                                hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
-                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64));
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half) {
-                                float lo, hi;
-                                bf16x2_to_acc(hv[2 * i + half], lo, hi);
-                                lo += __uint_as_float(v[4 * i + 2 * half]);
-                                hi += __uint_as_float(v[4 * i + 2 * half + 1]);
-                                hv[2 * i + half] = f32x2_to_bf16(lo, hi);
-                            }
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half)
-                                *reinterpret_cast<uint32_t*>(
-                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64)) =
-                                    hv[2 * i + half];
-                        tc::fence_proxy_async();
-                        __syncwarp();
-                        if (ch.y == kSpChunk) {
-                            if (lane == 0)
-                                tc::tma_store_2d_hint(&maps.y[s], j * kSpN + hf * 64, ch.x,
-                                                      sbase + panel + q * (kSpChunk * 128), stream);
-                        } else {
-                            __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y);
-                            for (int idx = lane; idx < ch.y * 8; idx += 32) {
-                                const int rr = idx >> 3, c16 = idx & 7;
-                                const uint4 val = *reinterpret_cast<const uint4*>(
-                                    sgen + panel + tc::sw128_offset(q * kSpChunk + rr, c16 * 8, 64));
-                                *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * a.site[s].ldy +
-                                                          j * kSpN + hf * 64 + c16 * 8) = val;
-                            }
+                    if (ch.y == kSpChunk) {
+                        if (lane == 0)
+                            tc::tma_store_2d_hint(&maps.y[s], j * kSpN + hf * 64, ch.x,
+                                                  sbase + panel + q * (kSpChunk * 128), stream);
+                    } else {
+                        __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y);
+                        for (int idx = lane; idx < ch.y * 8; idx += 32) {
+                            const int rr = idx >> 3, c16 = idx & 7;
+                            const uint4 val = *reinterpret_cast<const uint4*>(
+                                sgen + panel + tc::sw128_offset(q * kSpChunk + rr, c16 * 8, 64));
+                            *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * a.site[s].ldy +
+                                                      j * kSpN + hf * 64 + c16 * 8) = val;
                         }
                     }
-                    if (lane == 0) {
-                        tc::tma_store_commit();
-                        tc::tma_store_wait_read();
-                        tc::mbar_arrive(&empty[stage]);
-                    }
-                    __syncwarp();
-                    if (++stage == L::STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                    ++dc;
                 }
+                if (lane == 0) {
+                    // release the PREVIOUS stage once its store has read shared
+                    // memory: the store of this chunk drains while the next is processed
+                    tc::tma_store_commit();
+                    tc::tma_store_wait_read_1();
+                    if (pend >= 0) tc::mbar_arrive(&empty[pend]);
+                    pend = stage;
+                }
+                __syncwarp();
+                if (++stage == L::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+                ++dc;
             }
         }
-        if (lane == 0) tc::tma_store_wait_all();
+        if (lane == 0) {
+            tc::tma_store_wait_all();
+            if (pend >= 0) tc::mbar_arrive(&empty[pend]);
+        }
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -677,6 +754,9 @@ static int fill_common(SplitArgs& args, const preft_meta_t* meta, const preft_lo
     return PREFT_OK;
 }
 
+static long long* g_split_prof = nullptr;
+void split_set_profile(long long* buf) { g_split_prof = buf; }
+
 int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
                 const preft_lora_site_t* sites, int nsites, int r, int dtype, void* P, long long ldp,
                 cudaStream_t stream, int num_sms) {
@@ -705,13 +785,21 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
             if (!make_tmap_bf16_sw128(&maps.A[s], sites[s].A, 1ull << 20, static_cast<unsigned long long>(m),
                                       static_cast<unsigned long long>(m), 64, static_cast<unsigned>(r)))
                 return PREFT_ERR_CONFIG;
-        if (r == 16) {
-            if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, 192, maps, args, num_sms, stream);
-            if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, 192, maps, args, num_sms, stream);
-            return launch_tc(shrink_tc_kernel<16, 3>, ShrinkLayout<16, 3>::SMEM, 192, maps, args, num_sms, stream);
+        // two K halves per unit when the unit's K range is long enough to split
+        // (P must start at zero: the halves accumulate into it)
+        args.ks = getenv("PREFT_SPLIT_KS") ? atoi(getenv("PREFT_SPLIT_KS")) : 1;
+        args.prof = g_split_prof;
+        if (args.ks > 1) {
+            const cudaError_t e = cudaMemsetAsync(P, 0, static_cast<size_t>(rows) * ldp * sizeof(float), stream);
+            if (e != cudaSuccess) return -static_cast<int>(e);
         }
-        if (nsites == 1) return launch_tc(shrink_tc_kernel<32, 1>, ShrinkLayout<32, 1>::SMEM, 192, maps, args, num_sms, stream);
-        if (nsites == 2) return launch_tc(shrink_tc_kernel<32, 2>, ShrinkLayout<32, 2>::SMEM, 192, maps, args, num_sms, stream);
+        if (r == 16) {
+            if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, 224, maps, args, num_sms, stream);
+            if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, 224, maps, args, num_sms, stream);
+            return launch_tc(shrink_tc_kernel<16, 3>, ShrinkLayout<16, 3>::SMEM, 224, maps, args, num_sms, stream);
+        }
+        if (nsites == 1) return launch_tc(shrink_tc_kernel<32, 1>, ShrinkLayout<32, 1>::SMEM, 224, maps, args, num_sms, stream);
+        if (nsites == 2) return launch_tc(shrink_tc_kernel<32, 2>, ShrinkLayout<32, 2>::SMEM, 224, maps, args, num_sms, stream);
         return PREFT_ERR_RANK;  // 3 x 32 > 64 columns of P per row (checked above)
     }
     const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;

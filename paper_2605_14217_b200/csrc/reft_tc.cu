@@ -272,40 +272,41 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else if (warp == 0) {
         // ------------------------------------------------ shrink producer
-        if (lane == 0) {
-            const uint64_t keep = (a.flags & 16) ? tc::policy_evict_normal() : tc::policy_evict_last();
-            int stage = 0, ub = 0;
-            uint32_t phase = 0;
-            for (int u = u0; u < u1; ++u) {
-                const int4 U = a.units[u];
-                if (U.x < a.slot_base) continue;
-                const int slot = U.x - a.slot_base, nch = U.z;
-                // stay at most one unit ahead of the epilogue: the unit being
-                // re-read plus the one being streamed must fit in L2
-                if (ub > 0 && !(a.flags & 4)) tc::mbar_wait(&v_full[(ub - 1) & 1], ((ub - 1) >> 1) & 1);
-                ++ub;
-                int rows[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
-                const uint32_t bytes = static_cast<uint32_t>(nch * kChunk * 128 + L::AP_BYTES);
-                for (int p = 0; p < NP; ++p) {
+        // lane 0 owns the barriers; lane q issues chunk q's box and lane 4 the
+        // A panel, so a stage's boxes are in flight together (a single thread
+        // pays ~100+ cycles per TMA issue)
+        const uint64_t keep = tc::policy_evict_last();
+        int stage = 0, ub = 0;
+        uint32_t phase = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int4 U = a.units[u];
+            if (U.x < a.slot_base) continue;
+            const int slot = U.x - a.slot_base, nch = U.z;
+            // stay at most one unit ahead of the epilogue: the unit being
+            // re-read plus the one being streamed must fit in L2
+            if (lane == 0 && ub > 0 && !(a.flags & 4)) tc::mbar_wait(&v_full[(ub - 1) & 1], ((ub - 1) >> 1) & 1);
+            ++ub;
+            const int row = lane < nch ? a.chunks[U.y + lane].x : 0;
+            const uint32_t bytes = static_cast<uint32_t>(nch * kChunk * 128 + L::AP_BYTES);
+            for (int p = 0; p < NP; ++p) {
+                if (lane == 0) {
                     tc::mbar_wait(&sh_empty[stage], phase ^ 1u);
                     if ((a.flags & 2) && ub > 1) {
                         // panel p of this unit may load once the epilogue re-read columns p*64 - look*64 of the previous one
                         const int need = (ub - 2) * NJ + min(NJ, max(0, (p - a.look) * 64 / kEpiN + 1));
                         while (*reinterpret_cast<volatile int*>(&s_epi_done) < need) __nanosleep(64);
                     }
-                    const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
                     tc::mbar_expect_tx(&sh_full[stage], bytes);
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        if (q < nch)
-                            tc::tma_load_2d_hint(st + q * (kChunk * 128), &tmH, (pc0 + p) * 64, rows[q], &sh_full[stage], keep);
+                }
+                __syncwarp();
+                const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
+                if (lane < nch)
+                    tc::tma_load_2d_hint(st + lane * (kChunk * 128), &tmH, (pc0 + p) * 64, row, &sh_full[stage], keep);
+                else if (lane == 4)
                     tc::tma_load_2d(st + L::H_BYTES, &tmA, (pc0 + p) * 64, slot * R, &sh_full[stage]);
-                    if (++stage == L::SH_STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
+                if (++stage == L::SH_STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
             }
         }
@@ -348,22 +349,22 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else if (warp == 2) {
         // ------------------------------------------------ epilogue producer
-        if (lane == 0) {
-            const uint64_t stream = (a.flags & 16) ? tc::policy_evict_normal() : tc::policy_evict_first();
-            int stage = 0, ub = 0;
-            uint32_t phase = 0;
-            for (int u = u0; u < u1; ++u) {
-                const int4 U = a.units[u];
-                if (U.x < a.slot_base) continue;
-                const int slot = U.x - a.slot_base, nch = U.z;
-                const int unit_base = ub * NP;
-                ++ub;
-                int rows[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
-                const unsigned char* bt = a.Bt + static_cast<long long>(slot) * a.d * R * 2;
-                const uint32_t bytes = static_cast<uint32_t>(2 * nch * kChunk * 128 + L::BT_BYTES);
-                for (int j = 0; j < NJ; ++j) {
+        // lane 4*pp + q issues panel pp of chunk q, lane 8 the Bt chunk
+        const uint64_t stream = tc::policy_evict_first();
+        const int pp = lane >> 2, q = lane & 3;
+        int stage = 0, ub = 0;
+        uint32_t phase = 0;
+        for (int u = u0; u < u1; ++u) {
+            const int4 U = a.units[u];
+            if (U.x < a.slot_base) continue;
+            const int slot = U.x - a.slot_base, nch = U.z;
+            const int unit_base = ub * NP;
+            ++ub;
+            const int row = q < nch ? a.chunks[U.y + q].x : 0;
+            const unsigned char* bt = a.Bt + static_cast<long long>(slot) * a.d * R * 2;
+            const uint32_t bytes = static_cast<uint32_t>(2 * nch * kChunk * 128 + L::BT_BYTES);
+            for (int j = 0; j < NJ; ++j) {
+                if (lane == 0) {
                     tc::mbar_wait(&epi_empty[stage], phase ^ 1u);
                     if (!(a.flags & 8)) {
                         // never re-read columns before the shrink has read them: an
@@ -372,21 +373,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         const int need = unit_base + min(NP, (j + 1) * (kEpiN / 64));
                         while (*reinterpret_cast<volatile int*>(&s_shrunk) < need) __nanosleep(32);
                     }
-                    const uint32_t st = sbase + L::OFF_EPI + stage * L::EPI_STAGE;
                     tc::mbar_expect_tx(&epi_full[stage], bytes);
-#pragma unroll
-                    for (int pp = 0; pp < 2; ++pp)
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (q < nch)
-                                tc::tma_load_2d_hint(st + pp * L::H_BYTES + q * (kChunk * 128), &tmH,
-                                                     (jc0 + j) * kEpiN + pp * 64, rows[q], &epi_full[stage], stream);
+                }
+                __syncwarp();
+                const uint32_t st = sbase + L::OFF_EPI + stage * L::EPI_STAGE;
+                if (lane < 8 && q < nch)
+                    tc::tma_load_2d_hint(st + pp * L::H_BYTES + q * (kChunk * 128), &tmH, (jc0 + j) * kEpiN + pp * 64,
+                                         row, &epi_full[stage], stream);
+                else if (lane == 8)
                     tc::bulk_load_1d(st + L::EH_BYTES, bt + static_cast<long long>(jc0 + j) * L::BT_BYTES, L::BT_BYTES,
                                      &epi_full[stage]);
-                    if (++stage == L::EPI_STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
+                if (++stage == L::EPI_STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
             }
         }

@@ -1,0 +1,55 @@
+#!/usr/bin/env python
+"""Timeline of one tensor-core shrink launch (config-4 shapes, q/k/v group)."""
+import ctypes
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+
+
+def main():
+    import torch
+
+    import bench
+    from paper_2605_14217_b200 import AdapterKind, _lib, shapes
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.pool import AdapterPool
+    from paper_2605_14217_b200.tp import SplitWorkspace, apply_lora_group_tp_
+
+    dev = torch.device("cuda", 0)
+    shape = shapes.LLAMA_70B
+    pool = AdapterPool(1, shape.d_model, lora_sites=shape.site_dims(), lora_capacity=512, lora_rank=16,
+                       dtype=torch.bfloat16, device=dev, tp_rank=0, tp_size=8)
+    pool.fill_synthetic_(512, AdapterKind.LORA, 16, seed=1)
+    qsl, ids, flags, lens, _ = bench.step_entries(0, 1, 256, 256, seed=3)
+    slots = pool.entry_arrays(qsl, ids, flags)
+    T = int(qsl[-1])
+    meta = BatchMeta(len(ids), T, device=dev)
+    meta.set_slot_split(pool.slot_split)
+    meta.build_arrays(qsl, slots, flags)
+    print("units", meta.units_host().shape[0], "chunks", meta.chunks_host().shape[0], file=sys.stderr)
+    ws = SplitWorkspace(meta, pool)
+    group = ("Wq", "Wk", "Wv")
+    x = torch.randn(T, 8192, device=dev).to(torch.bfloat16)
+    ys = [torch.randn(T, pool.lora_shard[s].y_width, device=dev).to(torch.bfloat16) for s in group]
+    lib = _lib.load()
+    for _ in range(3):
+        apply_lora_group_tp_(ys, x, meta, pool, 0, group, workspace=ws, collective=False)
+    buf = torch.zeros(512, dtype=torch.int64, device=dev)
+    lib.preft_diag_split(ctypes.c_void_p(buf.data_ptr()))
+    apply_lora_group_tp_(ys, x, meta, pool, 0, group, workspace=ws, collective=False)
+    torch.cuda.synchronize()
+    lib.preft_diag_split(None)
+    st = buf.view(128, 4).cpu().numpy()
+    t0 = st[0, 0]
+    print("stage: producer_issue mma_consume | unit: s_full")
+    for i in range(64):
+        if st[i, 0] or st[i, 1] or st[i, 2]:
+            print(i, *(int(v - t0) if v else 0 for v in st[i, :3]))
+
+
+if __name__ == "__main__":
+    main()
