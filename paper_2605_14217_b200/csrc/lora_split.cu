@@ -177,7 +177,8 @@ __global__ void __launch_bounds__(256) expand_simt_kernel(const SplitArgs a) {
 constexpr int kSpU = 64;                  // unit rows (UMMA M)
 constexpr int kSpChunk = PREFT_CHUNK_ROWS;
 constexpr int kSpN = 128;                 // expand chunk width (UMMA N)
-constexpr int kSpAcc = 2;                 // split shrink accumulators
+constexpr int kSpAcc = 4;                 // split shrink accumulators = UMMA-issuing warps
+constexpr int kShrinkThreads = 32 * (6 + kSpAcc);
 
 struct SplitMaps {
     CUtensorMap x;     // x [rows][m] (this rank's columns), 16-row x 64-col boxes
@@ -195,11 +196,12 @@ struct ShrinkLayout {
     static constexpr int STAGES = STAGES_FIT > 16 ? 16 : STAGES_FIT;
     static constexpr int SMEM = STAGES * STAGE + 1024;
     static constexpr int TMEM_COLS = 2 * kSpAcc * NSR <= 256 ? 256 : 512;
+    static_assert(2 * kSpAcc * NSR <= 512, "TMEM budget");
 };
 
 // warps: 0 TMA producer (x), 6 TMA producer (A), 1 UMMA issuer, 2..5 TMEM -> P rows (lane quadrant = warp % 4)
 template <int R, int NS>
-__global__ void __launch_bounds__(224, 1) shrink_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
+__global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
     using L = ShrinkLayout<R, NS>;
     extern __shared__ unsigned char sm_raw[];
     __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
@@ -211,10 +213,10 @@ __global__ void __launch_bounds__(224, 1) shrink_tc_kernel(const __grid_constant
     if (tid == 32) {
         for (int i = 0; i < L::STAGES; ++i) {
             tc::mbar_init(&full[i], 1);
-            tc::mbar_init(&empty[i], 1);
+            tc::mbar_init(&empty[i], kSpAcc);  // one commit from each UMMA-issuing warp
         }
         for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&s_full[b], 1);
+            tc::mbar_init(&s_full[b], kSpAcc);
             tc::mbar_init(&s_empty[b], 4);
         }
         tc::fence_mbar_init();
@@ -284,7 +286,10 @@ __global__ void __launch_bounds__(224, 1) shrink_tc_kernel(const __grid_constant
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 1 || warp >= 7) {
+        // kSpAcc warps issue the UMMAs, K-step k into accumulator k % kSpAcc:
+        // one issuing thread is capped at ~140 cycles per UMMA
+        const int mw = warp == 1 ? 0 : warp - 6;
         if (lane == 0) {
             // the sites' A panels sit back to back in the stage, so one UMMA with
             // N = NS * R covers all of them (tiny-N UMMAs cost ~60-90 cycles each)
@@ -301,14 +306,14 @@ __global__ void __launch_bounds__(224, 1) shrink_tc_kernel(const __grid_constant
                 const uint32_t dS = tmem + sb * kSpAcc * L::NSR;
                 for (int p = p0; p < p1; ++p) {
                     tc::mbar_wait(&full[stage], phase);
-                    if (a.prof && blockIdx.x == 0 && nmc < 128) a.prof[nmc * 4 + 1] = clock64();
+                    if (a.prof && blockIdx.x == 0 && mw == 0 && nmc < 128) a.prof[nmc * 4 + 1] = clock64();
                     ++nmc;
                     tc::fence_after_sync();
                     const uint32_t st = sbase + stage * L::STAGE;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = mw; k < 4; k += kSpAcc) {
                         const int kk = (p - p0) * 4 + k;
-                        tc::mma_bf16(dS + (kk % kSpAcc) * L::NSR, tc::desc_kmajor_sw128(st + k * 32),
+                        tc::mma_bf16(dS + mw * L::NSR, tc::desc_kmajor_sw128(st + k * 32),
                                      tc::desc_kmajor_sw128(st + L::X_BYTES + k * 32), id, kk >= kSpAcc ? 1u : 0u);
                     }
                     tc::mma_commit(&empty[stage]);
@@ -794,12 +799,12 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
             if (e != cudaSuccess) return -static_cast<int>(e);
         }
         if (r == 16) {
-            if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, 224, maps, args, num_sms, stream);
-            if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, 224, maps, args, num_sms, stream);
-            return launch_tc(shrink_tc_kernel<16, 3>, ShrinkLayout<16, 3>::SMEM, 224, maps, args, num_sms, stream);
+            if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+            if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+            return launch_tc(shrink_tc_kernel<16, 3>, ShrinkLayout<16, 3>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
         }
-        if (nsites == 1) return launch_tc(shrink_tc_kernel<32, 1>, ShrinkLayout<32, 1>::SMEM, 224, maps, args, num_sms, stream);
-        if (nsites == 2) return launch_tc(shrink_tc_kernel<32, 2>, ShrinkLayout<32, 2>::SMEM, 224, maps, args, num_sms, stream);
+        if (nsites == 1) return launch_tc(shrink_tc_kernel<32, 1>, ShrinkLayout<32, 1>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+        if (nsites == 2) return launch_tc(shrink_tc_kernel<32, 2>, ShrinkLayout<32, 2>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
         return PREFT_ERR_RANK;  // 3 x 32 > 64 columns of P per row (checked above)
     }
     const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;
