@@ -176,7 +176,8 @@ __global__ void __launch_bounds__(256) expand_simt_kernel(const SplitArgs a) {
 
 constexpr int kSpU = 64;                  // unit rows (UMMA M)
 constexpr int kSpChunk = PREFT_CHUNK_ROWS;
-constexpr int kSpN = 128;                 // expand chunk width (UMMA N)
+constexpr int kSpN = 128;                 // expand chunk width (UMMA N) of narrow sites
+constexpr int kSpNMax = 256;              // expand chunk width of sites with n % 256 == 0
 constexpr int kSpAcc = 4;                 // split shrink accumulators = UMMA-issuing warps
 constexpr int kShrinkThreads = 32 * (6 + kSpAcc);
 
@@ -378,8 +379,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
 
 template <int R, int NS>
 struct ExpandLayout {
-    static constexpr int Y_BYTES = 2 * kSpU * 128;         // 64 rows x 128 cols (two swizzled panels)
-    static constexpr int BT_BYTES = kSpN * R * 2;
+    static constexpr int Y_BYTES = 4 * kSpU * 128;         // 64 rows x 256 cols (four swizzled panels)
+    static constexpr int BT_BYTES = kSpNMax * R * 2;
     static constexpr int STAGE = Y_BYTES + BT_BYTES;       // multiple of 1024
     static constexpr int V_BYTES = kSpU * R * 2;           // one V (hi or lo) of one site
     static constexpr int OFF_V = 0;                        // [2 buffers][NS sites][hi, lo]
@@ -387,6 +388,7 @@ struct ExpandLayout {
     static constexpr int STAGES_FIT = (227 * 1024 - 2048 - OFF_RING) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int SMEM = OFF_RING + STAGES * STAGE + 1024;
+    static_assert(STAGES >= 3, "expand ring too shallow");
 };
 
 // The expand's work item is (unit, block of kExpBlock 128-column chunks) over
@@ -400,11 +402,13 @@ struct ExpandItems {
     int ipu;     // items per unit
     int nc;      // chunks per unit (all sites)
     int off[4];  // first chunk of each site
+    int cw[3];   // chunk width of each site: 256 columns (one N = 256 UMMA), else 128
     __device__ void init(const SplitArgs& a, int nsites) {
         nc = 0;
         for (int s = 0; s < nsites; ++s) {
             off[s] = nc;
-            nc += a.site[s].n / kSpN;
+            cw[s] = a.site[s].n % kSpNMax == 0 ? kSpNMax : kSpN;
+            nc += a.site[s].n / cw[s];
         }
         off[nsites] = nc;
         ipu = (nc + kExpBlock - 1) / kExpBlock;
@@ -429,7 +433,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     const uint32_t raw = tc::smem_u32(sm_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
     unsigned char* sgen = sm_raw + (sbase - raw);
-    if (warp == 0) tc::tmem_alloc(&tslot, 256);
+    if (warp == 0) tc::tmem_alloc(&tslot, 512);
     if (tid == 32) {
         for (int i = 0; i < L::STAGES; ++i) {
             tc::mbar_init(&full[i], 1);
@@ -451,46 +455,46 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     it.init(a, NS);
 
     if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t stream = tc::policy_evict_first();
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int w = it.w0; w < it.w1; ++w) {
-                const int4 U = a.units[w / it.ipu];
-                if (U.x >= a.slot_base) continue;
-                const int nch = U.z;
-                int rows[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) rows[q] = q < nch ? a.chunks[U.y + q].x : 0;
-                const uint32_t bytes = static_cast<uint32_t>(2 * nch * kSpChunk * 128 + L::BT_BYTES);
-                const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
-                for (int c = c0; c < c1; ++c) {
-                    int s, j;
-                    it.site_of(c, NS, s, j);
-                    const unsigned char* bt = static_cast<const unsigned char*>(a.site[s].Bt_tc) +
-                                              static_cast<long long>(U.x) * a.site[s].n * R * 2;
+        // producer: lane 4*pp + q issues y panel pp of chunk q, lane 16 the Bt chunk
+        const uint64_t stream = tc::policy_evict_first();
+        const int pp = lane >> 2, q = lane & 3;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int w = it.w0; w < it.w1; ++w) {
+            const int4 U = a.units[w / it.ipu];
+            if (U.x >= a.slot_base) continue;
+            const int nch = U.z;
+            const int row = q < nch ? a.chunks[U.y + q].x : 0;
+            const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
+            for (int c = c0; c < c1; ++c) {
+                int s, j;
+                it.site_of(c, NS, s, j);
+                const int cw = it.cw[s];
+                const uint32_t bt_bytes = static_cast<uint32_t>(cw * R * 2);
+                if (lane == 0) {
                     tc::mbar_wait(&empty[stage], phase ^ 1u);
-                    const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
-                    tc::mbar_expect_tx(&full[stage], bytes);
-#pragma unroll
-                    for (int pp = 0; pp < 2; ++pp)
-#pragma unroll
-                        for (int q = 0; q < 4; ++q)
-                            if (q < nch)
-                                tc::tma_load_2d_hint(st + pp * kSpU * 128 + q * (kSpChunk * 128), &maps.y[s],
-                                                     j * kSpN + pp * 64, rows[q], &full[stage], stream);
-                    tc::bulk_load_1d(st + L::Y_BYTES, bt + static_cast<long long>(j) * L::BT_BYTES, L::BT_BYTES,
-                                     &full[stage]);
-                    if (++stage == L::STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
+                    tc::mbar_expect_tx(&full[stage], static_cast<uint32_t>((cw / 64) * nch * kSpChunk * 128) + bt_bytes);
+                }
+                __syncwarp();
+                const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
+                if (lane < 16 && pp < cw / 64 && q < nch)
+                    tc::tma_load_2d_hint(st + pp * kSpU * 128 + q * (kSpChunk * 128), &maps.y[s], j * cw + pp * 64, row,
+                                         &full[stage], stream);
+                else if (lane == 16)
+                    tc::bulk_load_1d(st + L::Y_BYTES,
+                                     static_cast<const unsigned char*>(a.site[s].Bt_tc) +
+                                         static_cast<long long>(U.x) * a.site[s].n * R * 2 +
+                                         static_cast<long long>(j) * bt_bytes,
+                                     bt_bytes, &full[stage]);
+                if (++stage == L::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            const uint32_t id = tc::idesc_bf16_f32(kSpU, kSpN);
+            const uint32_t id128 = tc::idesc_bf16_f32(kSpU, kSpN), id256 = tc::idesc_bf16_f32(kSpU, kSpNMax);
             int stage = 0, visit = 0, dc = 0, prev = -1;
             uint32_t phase = 0;
             for (int w = it.w0; w < it.w1; ++w) {
@@ -513,7 +517,8 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                     tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
                     tc::fence_after_sync();
                     const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
-                    const uint32_t dD = tmem + db * kSpN;
+                    const uint32_t dD = tmem + db * kSpNMax;
+                    const uint32_t id = it.cw[s] == kSpNMax ? id256 : id128;
 #pragma unroll
                     for (int k = 0; k < R / 16; ++k) {
                         const uint64_t bd = tc::desc_kmajor(bt + k * 256, 128, R * 16);
@@ -599,56 +604,67 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
             for (int c = c0; c < c1; ++c) {
                 int s, j;
                 it.site_of(c, NS, s, j);
+                const int cw = it.cw[s], npw = cw / 128;  // 64-column panels per warp: 1 or 2
                 const int db = dc & 1;
                 tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
                 tc::mbar_wait(&full[stage], phase);
                 tc::fence_after_sync();
-                uint32_t v[32];
-                tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpN + hf * 64, v);
+                uint32_t v[2][32];
+                tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpNMax + hf * (cw / 2), v[0]);
+                if (npw == 2) tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpNMax + hf * (cw / 2) + 64, v[1]);
                 tc::tmem_ld_wait();
                 tc::fence_before_sync();
                 __syncwarp();
                 if (lane == 0) tc::mbar_arrive(&d_empty[db]);
-                const uint32_t panel = L::OFF_RING + stage * L::STAGE + hf * kSpU * 128;
                 if (ch.y > 0) {
-                    uint32_t hv[16];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                    for (int pw = 0; pw < 2; ++pw) {
+                        if (pw >= npw) break;
+                        const int pan = hf * npw + pw;  // 64-column panel of the chunk
+                        const uint32_t panel = L::OFF_RING + stage * L::STAGE + pan * kSpU * 128;
+                        uint32_t hv[16];
 #pragma unroll
-                        for (int half = 0; half < 2; ++half)
-                            hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
-                                sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64));
+                        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                            for (int half = 0; half < 2; ++half)
+                                hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
+                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64));
 #pragma unroll
-                        for (int half = 0; half < 2; ++half) {
-                            float lo, hi;
-                            bf16x2_to_acc(hv[2 * i + half], lo, hi);
-                            lo += __uint_as_float(v[4 * i + 2 * half]);
-                            hi += __uint_as_float(v[4 * i + 2 * half + 1]);
-                            hv[2 * i + half] = f32x2_to_bf16(lo, hi);
-                        }
+                        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                            for (int half = 0; half < 2; ++half) {
+                                float lo, hi;
+                                bf16x2_to_acc(hv[2 * i + half], lo, hi);
+                                lo += __uint_as_float(v[pw][4 * i + 2 * half]);
+                                hi += __uint_as_float(v[pw][4 * i + 2 * half + 1]);
+                                hv[2 * i + half] = f32x2_to_bf16(lo, hi);
+                            }
 #pragma unroll
-                        for (int half = 0; half < 2; ++half)
-                            *reinterpret_cast<uint32_t*>(
-                                sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64)) =
-                                hv[2 * i + half];
+                        for (int i = 0; i < 8; ++i)
+#pragma unroll
+                            for (int half = 0; half < 2; ++half)
+                                *reinterpret_cast<uint32_t*>(
+                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64)) =
+                                    hv[2 * i + half];
+                    }
                     tc::fence_proxy_async();
                     __syncwarp();
-                    if (ch.y == kSpChunk) {
-                        if (lane == 0)
-                            tc::tma_store_2d_hint(&maps.y[s], j * kSpN + hf * 64, ch.x,
-                                                  sbase + panel + q * (kSpChunk * 128), stream);
-                    } else {
-                        __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y);
-                        for (int idx = lane; idx < ch.y * 8; idx += 32) {
-                            const int rr = idx >> 3, c16 = idx & 7;
-                            const uint4 val = *reinterpret_cast<const uint4*>(
-                                sgen + panel + tc::sw128_offset(q * kSpChunk + rr, c16 * 8, 64));
-                            *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * a.site[s].ldy +
-                                                      j * kSpN + hf * 64 + c16 * 8) = val;
+                    for (int pw = 0; pw < npw; ++pw) {
+                        const int pan = hf * npw + pw;
+                        const uint32_t panel = L::OFF_RING + stage * L::STAGE + pan * kSpU * 128;
+                        if (ch.y == kSpChunk) {
+                            if (lane == 0)
+                                tc::tma_store_2d_hint(&maps.y[s], j * cw + pan * 64, ch.x,
+                                                      sbase + panel + q * (kSpChunk * 128), stream);
+                        } else {
+                            __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y);
+                            for (int idx = lane; idx < ch.y * 8; idx += 32) {
+                                const int rr = idx >> 3, c16 = idx & 7;
+                                const uint4 val = *reinterpret_cast<const uint4*>(
+                                    sgen + panel + tc::sw128_offset(q * kSpChunk + rr, c16 * 8, 64));
+                                *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * a.site[s].ldy +
+                                                          j * cw + pan * 64 + c16 * 8) = val;
+                            }
                         }
                     }
                 }
@@ -677,7 +693,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     __syncthreads();
     if (warp == 0) {
         __syncwarp();
-        tc::tmem_dealloc(tmem, 256);
+        tc::tmem_dealloc(tmem, 512);
     }
 }
 
