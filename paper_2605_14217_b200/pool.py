@@ -41,7 +41,7 @@ from .adapters import AdapterKind, PositionSchedule
 from .batch import LORA_TARGETS, ForwardBatch, ModelAdapter
 from .errors import ConfigError, InfeasibleBatchError, RankError, ShapeError, StateError, SyncError
 
-__all__ = ["AdapterPool", "SlotInfo", "torch_dtype_code", "acc_dtype", "tile_kmajor", "untile_kmajor"]
+__all__ = ["AdapterPool", "SlotInfo", "SlotSnapshot", "torch_dtype_code", "acc_dtype", "tile_kmajor", "untile_kmajor"]
 
 _POW2 = (1, 2, 4, 8, 16, 32, 64)
 
@@ -80,6 +80,19 @@ def _round_rank(r: int) -> int:
         if r <= p:
             return p
     raise RankError(f"rank {r} exceeds the device limit 64")
+
+
+@dataclass
+class SlotSnapshot:
+    """Pinned host copy of one adapter's device slot (AdapterPool.export_slot)."""
+
+    info: "SlotInfo"
+    host: list
+    ready: object  # torch.cuda.Event recorded after the D2H copies
+
+    @property
+    def nbytes(self) -> int:
+        return sum(h.numel() * h.element_size() for h in self.host)
 
 
 @dataclass
@@ -248,11 +261,71 @@ class AdapterPool:
     def register_many(self, adapters: Iterable[ModelAdapter], stream=None) -> list[int]:
         return [self.register(a, stream) for a in adapters]
 
-    def unregister(self, adapter_id: int) -> None:
+    def unregister(self, adapter_id: int, zero: bool = True) -> None:
+        """Free an adapter's slot (zero=False leaves the stale weights for a
+        caller that overwrites the whole slot next, e.g. paging)."""
         info = self.info(adapter_id)
         del self._slots[adapter_id]
-        self._zero_slot(info)
+        if zero:
+            self._zero_slot(info)
         (self._free_lora if info.kind is AdapterKind.LORA else self._free_reft).append(info.slot)
+
+    # ------------------------------------------------------------ slot snapshots (paging)
+    def slot_views(self, kind: AdapterKind, slot: int) -> list[torch.Tensor]:
+        """Device views of every slab slice one slot owns, all layers."""
+        if kind is AdapterKind.LORA:
+            views = []
+            for name in self.lora_sites:
+                views += [self.lora_A[name][:, slot], self.lora_Bt[name][:, slot], self.lora_scale[name][:, slot]]
+                if name in self.lora_Bt_tc:
+                    views.append(self.lora_Bt_tc[name][:, slot])
+            return views
+        j = slot - self.slot_split
+        views = [self.reft_A[:, j], self.reft_B[:, j], self.reft_bias[:, j], self.reft_scale[:, j]]
+        if self.reft_Bt is not None:
+            views.append(self.reft_Bt[:, j])
+        return views
+
+    def export_slot(self, adapter_id: int, stream=None) -> "SlotSnapshot":
+        """Pinned host copy of an adapter's device slot (stream-ordered D2H)."""
+        info = self.info(adapter_id)
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        host = []
+        with torch.cuda.stream(s):
+            for v in self.slot_views(info.kind, info.slot):
+                h = torch.empty(v.shape, dtype=v.dtype, pin_memory=True)
+                h.copy_(v, non_blocking=True)
+                host.append(h)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        return SlotSnapshot(SlotInfo(adapter_id, -1, info.kind, info.rank, info.schedule, info.version), host, ev)
+
+    def import_slot(self, snap: "SlotSnapshot", stream=None) -> int:
+        """Place a snapshot into a free slot (stream-ordered H2D); returns the slot."""
+        info = snap.info
+        if info.adapter_id in self._slots:
+            raise StateError(f"adapter {info.adapter_id} is already resident")
+        free = self._free_lora if info.kind is AdapterKind.LORA else self._free_reft
+        if not free:
+            raise InfeasibleBatchError(f"no free {info.kind.value} slot (pool is full)")
+        slot = free.pop()
+        s = stream if stream is not None else torch.cuda.current_stream(self.device)
+        snap.ready.synchronize()  # the D2H that filled the snapshot has landed
+        with torch.cuda.stream(s):
+            for v, h in zip(self.slot_views(info.kind, slot), snap.host):
+                v.copy_(h, non_blocking=True)
+        self._slots[info.adapter_id] = SlotInfo(info.adapter_id, slot, info.kind, info.rank, info.schedule,
+                                                info.version)
+        return slot
+
+    @property
+    def lora_slot_bytes(self) -> int:
+        return sum(v.numel() * v.element_size() for v in self.slot_views(AdapterKind.LORA, 0)) if self.lora_capacity else 0
+
+    @property
+    def reft_slot_bytes(self) -> int:
+        return (sum(v.numel() * v.element_size() for v in self.slot_views(AdapterKind.DIREFT, self.slot_split))
+                if self.reft_capacity else 0)
 
     def sync(self, updates: Sequence[tuple[int, ModelAdapter]], stream=None) -> None:
         """Atomic weight sync at a step boundary (engine.py:676-697).
@@ -453,14 +526,24 @@ class AdapterPool:
         return meta.build(batch, self.slot_of, stream)
 
     def entry_arrays(self, qsl: np.ndarray, adapter_ids: Sequence[int | None], flags: np.ndarray) -> np.ndarray:
-        """Slot per entry for raw-array staging (unknown id -> BatchError)."""
+        """Slot per entry for raw-array staging.
+
+        An adapter that runs in the entry's phase must be resident (else
+        BatchError, as forward_chunk raises for ids missing from the catalogue,
+        model.py:470-472).  A PREFILL_ONLY adapter of a decode entry never runs
+        (engine.py:521-526), so it needs no slot: with paging it may well be
+        evicted, and the entry stages as adapter-less (the same mask)."""
         from .errors import BatchError
 
         out = np.full(len(adapter_ids), -1, dtype=np.int32)
+        flags = np.asarray(flags)
         for i, a in enumerate(adapter_ids):
             if a is not None:
                 info = self._slots.get(a)
                 if info is None:
-                    raise BatchError(f"adapter {a} not in catalogue")
+                    runs = not (flags[i] & _lib.ENTRY_DECODE) or bool(flags[i] & _lib.ENTRY_ALL_POSITIONS)
+                    if runs:
+                        raise BatchError(f"adapter {a} not in catalogue")
+                    continue
                 out[i] = info.slot
         return out
