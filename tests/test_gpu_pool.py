@@ -122,3 +122,28 @@ def test_graph_replay_sees_synced_weights_and_new_batches(cuda_device):
     replay_and_check(qsl, ids, flags)
     qsl2, ids2, flags2 = U.random_entries(rng, 9, [0, 1, 2], max_len=20)
     replay_and_check(qsl2, ids2, flags2)
+
+
+def test_register_from_adp1_directory_matches_in_memory(cuda_device, tmp_path):
+    """The ADP1 bulk loader fills the pool with exactly the bits of the
+    in-memory bundle it was saved from (LoRA with the tiled tensor-core copy,
+    and ReFT)."""
+    import gpu_util as U
+    from paper_2605_14217_b200 import AdapterKind
+    from paper_2605_14217_b200.adapter_io import register_dir, save_model_adapter
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(4)
+    sites = {"Wq": (256, 128), "Wk": (128, 128)}
+    lora = U.random_lora_adapter(rng, 11, 2, sites, 16)
+    reft = U.random_reft_adapter(rng, 12, 2, 128, 16, AdapterKind.DIREFT)
+    pools = [AdapterPool(2, 128, lora_sites=sites, lora_capacity=2, lora_rank=16, reft_capacity=2, reft_rank=16,
+                         dtype=torch.bfloat16, device=cuda_device) for _ in range(2)]
+    for a in (lora, reft):
+        pools[0].register(a)
+        register_dir(pools[1], save_model_adapter(a, tmp_path / str(a.adapter_id)))
+    torch.cuda.synchronize()
+    for a in (lora, reft):
+        va = pools[0].slot_views(a.kind, pools[0].info(a.adapter_id).slot)
+        vb = pools[1].slot_views(a.kind, pools[1].info(a.adapter_id).slot)
+        assert all(torch.equal(x, y) for x, y in zip(va, vb))

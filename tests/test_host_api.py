@@ -195,3 +195,42 @@ def test_routing_covers_every_request_once():
                     assert owner_of(a, world) == r
         if world == 8:
             assert 0 in reps  # adapter 0 carries ~14.7% > 1/8 of the Zipf load
+
+
+def test_adapter_directory_round_trip_bit_exact(tmp_path):
+    """ADP1 directories (adapter_io.py): every bundle of a LoRA and a ReFT
+    ModelAdapter survives save/load bit for bit (adapters.py:391-436)."""
+    import gpu_util as U
+    from paper_2605_14217_b200 import AdapterKind
+    from paper_2605_14217_b200.adapter_io import load_catalogue, load_model_adapter, save_model_adapter
+
+    rng = np.random.default_rng(9)
+    lora = U.random_lora_adapter(rng, 3, 2, {"Wq": (16, 8), "Wdown": (8, 24)}, 4)
+    reft = U.random_reft_adapter(rng, 5, 3, 8, 2, AdapterKind.LOREFT)
+    for a in (lora, reft):
+        save_model_adapter(a, tmp_path / f"a{a.adapter_id}")
+        b = load_model_adapter(tmp_path / f"a{a.adapter_id}")
+        assert (b.adapter_id, b.kind, b.rank, b.schedule) == (a.adapter_id, a.kind, a.rank, a.schedule)
+        pa = sorted(a.lora_sites.items()) if a.kind is AdapterKind.LORA else list(enumerate(a.reft_sites))
+        pb = sorted(b.lora_sites.items()) if b.kind is AdapterKind.LORA else list(enumerate(b.reft_sites))
+        assert [k for k, _ in pa] == [k for k, _ in pb]
+        for (_, x), (_, y) in zip(pa, pb):
+            assert x.dims == y.dims and x.scaling == y.scaling
+            for tx, ty in zip(x.tensors, y.tensors):
+                assert tx.tobytes() == ty.tobytes()
+    assert sorted(load_catalogue(tmp_path)) == [3, 5]
+
+
+def test_adapter_directory_rejects_corruption(tmp_path):
+    import gpu_util as U
+    from paper_2605_14217_b200.adapter_io import load_model_adapter, save_model_adapter
+    from paper_2605_14217_b200.errors import ShapeError
+
+    rng = np.random.default_rng(1)
+    d = save_model_adapter(U.random_lora_adapter(rng, 1, 1, {"Wq": (8, 8)}, 2), tmp_path / "a")
+    f = d / "L0_Wq.adp1"
+    f.write_bytes(f.read_bytes()[:-3])
+    with pytest.raises(ShapeError):
+        load_model_adapter(d)
+    with pytest.raises(ShapeError):
+        load_model_adapter(tmp_path / "missing")
