@@ -613,6 +613,92 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
     return out
 
 
+def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dict:
+    """the reference engine's schedule replayed on the
+    device — Uniform Punica requests over 512 LoRA^P r=1 adapters (8B shapes),
+    max_batch 32, at most 32 adapters resident (paged with LRU from pinned
+    host slot images), token budget 2048, decode-first mixed
+    batches; per step: paging, K1 from the new entries, 32 layers x 4 fused
+    LoRA groups through the native step plan.  Tokens/s counts every token
+    the steps process (prompt + generated), device time of the whole run."""
+    import torch
+
+    from paper_2605_14217_b200 import AdapterKind, shapes
+    from paper_2605_14217_b200.adapters import PositionSchedule
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.paging import PagedAdapterPool
+    from paper_2605_14217_b200.plan import StepPlan
+    from paper_2605_14217_b200.pool import AdapterPool
+    from paper_2605_14217_b200.serving import Scheduler, ServeConfig, generate_workload
+    from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig
+
+    shape = shapes.LLAMA_8B
+    slots = 32
+    pool = AdapterPool(N_LAYERS, shape.d_model, lora_sites=shape.site_dims(), lora_capacity=slots, lora_rank=RANK,
+                       dtype=torch.bfloat16, device=device)
+    snaps = {}
+    for first in range(0, N_ADAPTERS, slots):  # pinned host slot images of all 512 adapters
+        ids = list(range(first, min(N_ADAPTERS, first + slots)))
+        pool.fill_synthetic_(0, AdapterKind.LORA, RANK, seed=100 + first, sigma=0.01, ids=ids)
+        for a in ids:
+            snaps[a] = pool.export_slot(a)
+        torch.cuda.synchronize()
+        for a in ids:
+            pool.unregister(a, zero=False)
+    paged = PagedAdapterPool(pool, {}, snapshots=snaps)
+    cfg = ServeConfig(max_batch=32, max_gpu_adapters=slots, step_token_budget=2048)
+    meta = BatchMeta(cfg.max_batch, cfg.step_token_budget, tile_tokens=128, device=device)
+    dims = shape.site_dims()
+    g = torch.Generator(device=device)
+    g.manual_seed(5)
+    T = cfg.step_token_budget
+    plan = StepPlan(meta, pool, max_tokens=T)
+    for layer in range(N_LAYERS):
+        for group in shapes.SITE_GROUPS:
+            x = torch.randn(T, dims[group[0]][1], generator=g, device=device).to(torch.bfloat16)
+            ys = [torch.randn(T, dims[t][0], generator=g, device=device).to(torch.bfloat16) for t in group]
+            plan.add_lora_group(ys, x, layer, group)
+    wl = generate_workload(WorkloadConfig(n_requests, N_ADAPTERS, AdapterMix.UNIFORM, seed=0, l_max=l_max))
+    s = torch.cuda.current_stream(device)
+    from paper_2605_14217_b200 import _lib
+
+    def run(limit=None):
+        steps = toks = pre = 0
+        for step in Scheduler(wl, cfg, PositionSchedule.PREFILL_ONLY):
+            paged.ensure(step.workset, stream=s)
+            # all-unselected steps skip the adapter path, decided on the host
+            # (forward_chunk's skip_adapters, model.py:475): decode-only steps
+            # of prefill-only adapters launch nothing
+            if any(a is not None and not d for a, d in zip(step.adapter_ids, step.decode_flags)):
+                flags = (step.decode_flags * _lib.ENTRY_DECODE).astype(np.int32)
+                meta.build_arrays(step.qsl, pool.entry_arrays(step.qsl, step.adapter_ids, flags), flags, stream=s)
+                plan.run(s, run_meta=False)
+            steps += 1
+            toks += step.tokens
+            pre += step.prefill_tokens
+            if limit and steps >= limit:
+                break
+        return steps, toks, pre
+
+    run(limit=5)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    p0, b0 = paged.page_ins, paged.paged_bytes
+    e0.record(s)
+    steps, toks, pre = run()
+    e1.record(s)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out = {"workload": f"serving replay: Uniform Punica {n_requests} requests (l_max {l_max}) over 512 LoRA^P r1 "
+                       f"adapters, 8B shapes x 32 layers, max_batch 32, 32 device slots (LRU paging), budget 2048",
+           "steps": steps, "tokens": toks, "prefill_tokens": pre, "ms": round(ms, 2),
+           "value": round(toks / (ms / 1e3), 1), "unit": "tokens/s (prompt + generated)",
+           "page_ins": paged.page_ins - p0, "paged_gb": round((paged.paged_bytes - b0) / 1e9, 2)}
+    del plan, pool, paged, snaps
+    torch.cuda.empty_cache()
+    return out
+
+
 def secondary_configs(args, device) -> list:
     from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig, assign_adapters
 
@@ -626,6 +712,7 @@ def secondary_configs(args, device) -> list:
     lens5 = rng.integers(8192, 16385, size=8)
     out.append(reft_config(args, device, "loreft", 32, lens5, ids5,
                            "cfg5 slice (1 GPU): Zipf over 512 adapters, 8 prompts U[8k,16k], LoReFT^P r32 x 32 layers"))
+    out.append(serving_replay(args, device))
     return out
 
 

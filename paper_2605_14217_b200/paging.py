@@ -79,22 +79,25 @@ class PagedAdapterPool:
     """An `AdapterPool` fronted by a host catalogue larger than its slots."""
 
     def __init__(self, pool, catalogue: Mapping[int, ModelAdapter], lora_capacity: int | None = None,
-                 reft_capacity: int | None = None):
+                 reft_capacity: int | None = None, snapshots: Mapping[int, object] | None = None):
         self.pool = pool
         self.catalogue = dict(catalogue)
+        self._kinds = {aid: a.kind for aid, a in self.catalogue.items()}
+        for aid, snap in (snapshots or {}).items():  # pre-converted slot images (SlotSnapshot)
+            self._kinds[aid] = snap.info.kind
         lc = pool.lora_capacity if lora_capacity is None else int(lora_capacity)
         rc = pool.reft_capacity if reft_capacity is None else int(reft_capacity)
         if lc > pool.lora_capacity or rc > pool.reft_capacity:
             raise ConfigError("paging capacity exceeds the pool's slots")
         self._lru = {True: LruResidency(lc) if lc else None, False: LruResidency(rc) if rc else None}
-        self._snap: dict[int, object] = {}  # adapter id -> pinned SlotSnapshot
+        self._snap: dict[int, object] = dict(snapshots or {})  # adapter id -> pinned SlotSnapshot
         self.paged_bytes = 0
         self.page_ins = 0
         self.evictions = 0
 
     def byte_size(self, adapter_id: int) -> int:
         """Device bytes of one adapter's slot (what a page-in moves)."""
-        lora = self.catalogue[adapter_id].kind is AdapterKind.LORA
+        lora = self._kinds[adapter_id] is AdapterKind.LORA
         return self.pool.lora_slot_bytes if lora else self.pool.reft_slot_bytes
 
     @property
@@ -108,11 +111,11 @@ class PagedAdapterPool:
     def ensure(self, needed: Sequence[int], stream=None) -> tuple[list[int], list[int], int]:
         """Make every adapter of the step resident (engine.py:412-418)."""
         for aid in needed:
-            if aid not in self.catalogue:
+            if aid not in self._kinds:
                 raise StateError(f"adapter {aid} is not in the catalogue")
         paged, evicted, moved = [], [], 0
         for lora in (True, False):
-            ids = [a for a in needed if (self.catalogue[a].kind is AdapterKind.LORA) == lora]
+            ids = [a for a in needed if (self._kinds[a] is AdapterKind.LORA) == lora]
             if not ids:
                 continue
             lru = self._lru[lora]
@@ -141,6 +144,7 @@ class PagedAdapterPool:
         """Weight sync for a paged catalogue: resident adapters are overwritten
         in place (AdapterPool.sync), non-resident ones on their next page-in."""
         self.catalogue[adapter_id] = adapter
+        self._kinds[adapter_id] = adapter.kind
         self._snap.pop(adapter_id, None)
         if adapter_id in self.pool:
             self.pool.sync([(adapter_id, adapter)], stream)

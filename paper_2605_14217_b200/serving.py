@@ -229,6 +229,13 @@ class ServingLoop:
         e0.record(s)
         for step in scheduler:
             self.paged.ensure(step.workset, stream=s)
+            if not step.workset:
+                # nothing executes (forward_chunk's skip_adapters, model.py:475)
+                steps += 1
+                tokens += step.tokens
+                if max_steps is not None and steps >= max_steps:
+                    break
+                continue
             flags = step.decode_flags * _lib.ENTRY_DECODE
             if self._schedule_of is not None:
                 allp = [a is not None and self._schedule_of(a) is PositionSchedule.ALL_POSITIONS
