@@ -568,21 +568,31 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
     for _ in range(2):
         step(s)
     torch.cuda.synchronize()
+    launch = "cuda graph"
     graph = torch.cuda.CUDAGraph()
-    cs = torch.cuda.Stream(device)
-    cs.wait_stream(s)
-    with torch.cuda.stream(cs):
-        with torch.cuda.graph(graph, stream=cs):
-            step(cs)
-    s.wait_stream(cs)
+    try:
+        cs = torch.cuda.Stream(device)
+        cs.wait_stream(s)
+        with torch.cuda.stream(cs):
+            with torch.cuda.graph(graph, stream=cs):
+                step(cs)
+        s.wait_stream(cs)
+        replay = graph.replay
+    except Exception as exc:  # e.g. a collective that refuses capture: time the eager launches
+        torch.cuda.synchronize()
+        launch = f"eager (graph capture failed: {type(exc).__name__})"
+        graph = None
+
+        def replay():
+            step(s)
     for _ in range(2):
-        graph.replay()
+        replay()
     torch.cuda.synchronize()
     barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     for _ in range(steps):
-        graph.replay()
+        replay()
     e1.record(s)
     torch.cuda.synchronize()
     ms = all_max(e0.elapsed_time(e1) / steps, world)
@@ -607,7 +617,7 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
            "prefill_tokens": sel, "ms_per_step": round(ms, 3), "value": round(sel / (ms / 1e3), 1), "unit": UNIT,
            "per_rank_frac_of_hbm_peak": round(frac, 4), "per_rank_algorithmic_bytes": int(step_bytes),
            "allreduce_bytes_per_rank_per_step": int(allreduce_bytes) if real else 0,
-           "pool_gb_per_rank": round(pool.nbytes / 1e9, 2), "launch": "cuda graph"}
+           "pool_gb_per_rank": round(pool.nbytes / 1e9, 2), "launch": launch}
     del pool, meta, ws, sets, graph
     torch.cuda.empty_cache()
     return out
@@ -773,7 +783,11 @@ def run_ours(args):
         del ctx["plan"], ctx["acts"]
         torch.cuda.empty_cache()
         others = secondary_configs(args, device) if world == 1 else []
-        cfg4 = tp_config(args, device, world, rank)
+        try:
+            cfg4 = tp_config(args, device, world, rank)
+        except Exception as exc:  # never lose the headline line to the secondary config
+            cfg4 = {"workload": "cfg4 (70B, TP=8)", "error": f"{type(exc).__name__}: {exc}"[:300]}
+            torch.cuda.empty_cache()
         if cfg4 is not None:
             others.append(cfg4)
     cpu = None
