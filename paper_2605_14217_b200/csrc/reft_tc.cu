@@ -95,7 +95,8 @@ struct ReftTcArgs {
     const int* counters;
     int flags;  // diagnostics knobs: bit 0 immediate stage release, bit 1 pace the shrink behind the
                 // epilogue, bit 2 no one-unit throttle of the shrink, bit 3 let the
-                // epilogue producer read ahead of the shrink
+                // epilogue producer read ahead of the shrink, bit 4 no L2 hints, bit 5
+                // reduce epilogue (bf16 delta added into h by TMA in L2, no re-read)
     int look;   // with bit 1: panels the shrink may run ahead of the epilogue's re-read
     long long* prof;  // diagnostics: clock64 stamps of CTA 0 (NULL in production)
 };
@@ -362,11 +363,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             ++ub;
             const int row = q < nch ? a.chunks[U.y + q].x : 0;
             const unsigned char* bt = a.Bt + static_cast<long long>(slot) * a.d * R * 2;
-            const uint32_t bytes = static_cast<uint32_t>(2 * nch * kChunk * 128 + L::BT_BYTES);
+            const bool reduce = a.flags & 32;  // epilogue adds delta in L2: no re-read of h
+            const uint32_t bytes = static_cast<uint32_t>((reduce ? 0 : 2 * nch * kChunk * 128) + L::BT_BYTES);
             for (int j = 0; j < NJ; ++j) {
                 if (lane == 0) {
                     tc::mbar_wait(&epi_empty[stage], phase ^ 1u);
-                    if (!(a.flags & 8)) {
+                    if (!(a.flags & 8) && !reduce) {
                         // never re-read columns before the shrink has read them: an
                         // early (evict_first) epilogue read would miss, and could
                         // evict the lines before the shrink gets to them
@@ -377,7 +379,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 }
                 __syncwarp();
                 const uint32_t st = sbase + L::OFF_EPI + stage * L::EPI_STAGE;
-                if (lane < 8 && q < nch)
+                if (lane < 8 && q < nch && !reduce)
                     tc::tma_load_2d_hint(st + pp * L::H_BYTES + q * (kChunk * 128), &tmH, (jc0 + j) * kEpiN + pp * 64,
                                          row, &epi_full[stage], stream);
                 else if (lane == 8)
@@ -460,7 +462,25 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 if (lane == 0) tc::mbar_arrive(&d_empty[db]);
                 PROF(5);
                 const uint32_t panel = L::OFF_EPI + stage * L::EPI_STAGE + hf * L::H_BYTES;
-                if (ch.y > 0) {
+                if (ch.y > 0 && (a.flags & 32)) {
+                    // reduce epilogue: stage the bf16 delta (-0.0 in rows past the
+                    // chunk: the additive identity that keeps every bit, -0.0
+                    // included) and let TMA add it into h in L2
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int half = 0; half < 2; ++half) {
+                            const int rr = r1 + 8 * half;
+                            const uint32_t d = rr < ch.y ? f32x2_to_bf16(__uint_as_float(v[4 * i + 2 * half]),
+                                                                          __uint_as_float(v[4 * i + 2 * half + 1]))
+                                                         : 0x80008000u;
+                            *reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(q * kChunk + rr, 8 * i + cp, 64)) = d;
+                        }
+                    tc::fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0)
+                        tc::tma_reduce_add_2d(&tmH, (jc0 + j) * kEpiN + hf * 64, ch.x, sbase + panel + q * (kChunk * 128));
+                } else if (ch.y > 0) {
                     // all 16 loads first, then the math, then the stores (the
                     // addresses are disjoint but not provably so to the compiler)
                     uint32_t hv[16];

@@ -200,6 +200,15 @@ __device__ __forceinline__ void tma_store_2d_hint(const void* tmap, int c0, int 
                  : "memory");
 }
 
+// 2D tensor-map reduce-add of one box from shared memory into global memory
+// (the add happens in L2; bulk async group, like a TMA store)
+__device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, int c0, int c1, uint32_t ssrc) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(ssrc)
+                 : "memory");
+}
+
 // contiguous global -> shared bulk copy (bytes % 16 == 0, 16 B aligned), completion on an mbarrier
 __device__ __forceinline__ void bulk_load_1d(uint32_t sdst, const void* gsrc, uint32_t bytes, uint64_t* mbar) {
     asm volatile(
