@@ -243,6 +243,15 @@ int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ld
  * only (PREFT_ERR_SHAPE when ineligible).  Env: PREFT_REFT_VARIANT=simt|tc. */
 int preft_set_reft_variant(int32_t variant);
 
+/* Tensor-core ReFT pipeline knobs (diagnostics / A-B measurement; results
+ * never change): bit 0 immediate ring-stage release, bit 1 pace the shrink
+ * behind the epilogue (`look` panels ahead, -1 = 3/4 of a unit), bit 2 no
+ * one-unit throttle, bit 3 let the epilogue re-read run ahead of the shrink,
+ * bit 4 no L2 cache hints, bit 5 reduce epilogue (TMA adds the bf16 delta
+ * into h in L2 instead of re-reading h).  flags = -1 restores the default
+ * (environment PREFT_REFT_TC_FLAGS / PREFT_REFT_TC_LOOK, else 7). */
+int preft_set_reft_tc_flags(int32_t flags, int32_t look);
+
 /*
  * K4: dst[i*dst_ld + j] = convert(src[i*src_stride_row + j*src_stride_col])
  * for i < rows_valid, j < cols; rows in [rows_valid, rows) are zero-filled.

@@ -121,6 +121,7 @@ SIGNATURES = {
         ],
     ),
     "preft_set_reft_variant": (ctypes.c_int, [ctypes.c_int32]),
+    "preft_set_reft_tc_flags": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32]),
     "preft_lora_shrink": (
         ctypes.c_int,
         [

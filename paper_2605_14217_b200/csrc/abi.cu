@@ -24,6 +24,7 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
                 int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
 int reft_tc_last_grid();
 void reft_tc_set_profile(long long* buf);
+void reft_tc_set_flags(int flags, int look);
 
 static thread_local char g_last_cuda_error[256] = "";
 
@@ -199,6 +200,12 @@ int preft_set_split_variant(int32_t variant) {
 int preft_diag_reft_tc(long long* device_buffer) {
     reft_tc_set_profile(device_buffer);
     return reft_tc_last_grid();
+}
+
+int preft_set_reft_tc_flags(int32_t flags, int32_t look) {
+    if (flags < -1 || flags > 127) return PREFT_ERR_DOMAIN;
+    reft_tc_set_flags(flags, look);
+    return PREFT_OK;
 }
 
 int preft_set_reft_variant(int32_t variant) {

@@ -563,6 +563,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 static int g_tc_last_grid = 0;
+static int g_tc_flags = -1, g_tc_look = -1;  // -1: from the environment (PREFT_REFT_TC_FLAGS / _LOOK)
+void reft_tc_set_flags(int flags, int look) {
+    g_tc_flags = flags;
+    g_tc_look = look;
+}
 static long long* g_tc_prof = nullptr;
 int reft_tc_last_grid() { return g_tc_last_grid; }
 void reft_tc_set_profile(long long* buf) { g_tc_prof = buf; }
@@ -646,7 +651,8 @@ int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long l
     args.units = reinterpret_cast<const int4*>(meta->units);
     args.counters = meta->counters;
     {
-        static int flags = -1, look = 0;
+        int& flags = g_tc_flags;
+        int& look = g_tc_look;
         if (flags < 0) {
             const char* f = getenv("PREFT_REFT_TC_FLAGS");
             const char* l = getenv("PREFT_REFT_TC_LOOK");

@@ -158,3 +158,42 @@ def test_tiled_bt_is_b_transposed(cuda_device):
     pool.register(U.random_reft_adapter(rng, 8, 2, 256, 8, AdapterKind.LOREFT))
     pool.fill_synthetic_(2, AdapterKind.DIREFT, 16, first_id=20)
     assert torch.equal(untile_kmajor(pool.reft_Bt), pool.reft_B.transpose(-1, -2))
+
+
+@pytest.mark.parametrize("flags", [39, 5, 45])
+def test_tensor_core_pipeline_knobs_keep_results(cuda_device, flags):
+    """The K3-TC pipeline knobs (reduce epilogue, unpaced shrink, early
+    re-read) change scheduling only: same parity, unselected rows untouched."""
+    from paper_2605_14217_b200 import _lib
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_reft_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(flags)
+    d = 2048
+    pool = AdapterPool(1, d, reft_capacity=4, reft_rank=16, dtype=torch.bfloat16, device=cuda_device)
+    for aid in range(4):
+        pool.register(U.random_reft_adapter(rng, aid, 1, d, 16, AdapterKind.DIREFT if aid % 2 else AdapterKind.LOREFT))
+    lens = [1] * 6 + list(rng.integers(1, 60, size=10)) + [300, 257]
+    qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    ids = [int(i) % 4 if i % 7 else None for i in range(len(lens))]
+    flags_e = np.array([_lib.ENTRY_DECODE] * 6 + [0] * (len(lens) - 6), dtype=np.int32)
+    meta = BatchMeta(32, int(qsl[-1]), device=cuda_device)
+    slots = U.stage(meta, pool, qsl, ids, flags_e)
+    h = U.rand_act(rng, int(qsl[-1]), d, torch.bfloat16, cuda_device)
+    h[3, 5] = -0.0  # a negative zero in an unselected row must survive the reduce epilogue
+    h_in = U.to_np(h)
+    neg0 = h[3, 5].clone()
+    lib = _lib.load()
+    assert lib.preft_set_reft_tc_flags(flags, -1) == 0
+    try:
+        apply_reft_(h, meta, pool, 0)
+        torch.cuda.synchronize()
+    finally:
+        lib.preft_set_reft_tc_flags(-1, -1)
+    mask = U.oracle_mask(qsl, slots, flags_e)
+    out = U.to_np(h)
+    assert np.array_equal(out[~mask], h_in[~mask])
+    assert torch.equal(h[3, 5].view(torch.int16), neg0.view(torch.int16))
+    ref = U.reft_oracle(h_in, qsl, slots, flags_e, pool, 0)
+    helpers.check_close(out, h_in, ref, "bf16", f"reft knobs {flags}")
