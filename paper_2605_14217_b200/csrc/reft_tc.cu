@@ -295,7 +295,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     if ((a.flags & 2) && ub > 1) {
                         // panel p of this unit may load once the epilogue re-read columns p*64 - look*64 of the previous one
                         const int need = (ub - 2) * NJ + min(NJ, max(0, (p - a.look) * 64 / kEpiN + 1));
-                        while (*reinterpret_cast<volatile int*>(&s_epi_done) < need) __nanosleep(64);
+                        while (atomicOr(&s_epi_done, 0) < need) __nanosleep(64);
                     }
                     tc::mbar_expect_tx(&sh_full[stage], bytes);
                 }
@@ -327,7 +327,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 for (int p = 0; p < NP; ++p) {
                     tc::mbar_wait(&sh_full[stage], phase);
                     // these rows are in L2 now: the epilogue producer may re-read them
-                    *reinterpret_cast<volatile int*>(&s_shrunk) = (ub * NP) + p + 1;
+                    atomicMax(&s_shrunk, (ub * NP) + p + 1);  // shared-memory atomics: an explicit, race-free flag
                     if (a.prof && blockIdx.x == 0 && ub < 16 && (p == 0 || p == NP - 1))
                         a.prof[576 + ub * 2 + (p ? 1 : 0)] = clock64();
                     tc::fence_after_sync();
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         // early (evict_first) epilogue read would miss, and could
                         // evict the lines before the shrink gets to them
                         const int need = unit_base + min(NP, (j + 1) * (kEpiN / 64));
-                        while (*reinterpret_cast<volatile int*>(&s_shrunk) < need) __nanosleep(32);
+                        while (atomicOr(&s_shrunk, 0) < need) __nanosleep(32);
                     }
                     tc::mbar_expect_tx(&epi_full[stage], bytes);
                 }
@@ -536,7 +536,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         if (pend >= 0) tc::mbar_arrive(&epi_empty[pend]);
                         pend = stage;
                     }
-                    if (warp == 4) *reinterpret_cast<volatile int*>(&s_epi_done) = s_epi_done + 1;
+                    if (warp == 4) atomicAdd(&s_epi_done, 1);
                 }
                 __syncwarp();
                 PROF(7);

@@ -1,0 +1,52 @@
+#!/usr/bin/env python
+"""Small invocations of every kernel family for compute-sanitizer runs:
+K1, K2 (team, warp, f64), K2 split (tcgen05 + SIMT), K3 (SIMT + tcgen05), K4."""
+import sys
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parents[1]
+sys.path.insert(0, str(ROOT))
+sys.path.insert(0, str(ROOT / "tests"))
+
+
+def main():
+    import torch
+
+    import gpu_util as U
+    from paper_2605_14217_b200 import AdapterKind, _lib
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_group_, apply_reft_
+    from paper_2605_14217_b200.pool import AdapterPool
+    from paper_2605_14217_b200.tp import SplitWorkspace, apply_lora_group_tp_
+
+    dev = torch.device("cuda", 0)
+    rng = np.random.default_rng(0)
+    for dtype, lr, rr in ((torch.bfloat16, 1, 16), (torch.bfloat16, 16, 32), (torch.float64, 2, 4)):
+        d = 256
+        sites = {"Wq": (d, d), "Wk": (128, d), "Wv": (128, d)}
+        pool = AdapterPool(1, d, lora_sites=sites, lora_capacity=3, lora_rank=lr, reft_capacity=3, reft_rank=rr,
+                           dtype=dtype, device=dev)
+        for a in range(3):
+            pool.register(U.random_lora_adapter(rng, a, 1, sites, lr))
+            pool.register(U.random_reft_adapter(rng, 10 + a, 1, d, rr, AdapterKind.DIREFT))
+        lens = [1] * 4 + list(rng.integers(1, 70, size=8)) + [150]
+        qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        ids = [[0, 1, 2, 10, 11, 12, None][int(i) % 7] for i in range(len(lens))]
+        flags = np.array([_lib.ENTRY_DECODE] * 4 + [0] * (len(lens) - 4), np.int32)
+        meta = BatchMeta(32, int(qsl[-1]), device=dev)
+        U.stage(meta, pool, qsl, ids, flags)
+        T = int(qsl[-1])
+        x = U.rand_act(rng, T, d, dtype, dev)
+        ys = [U.rand_act(rng, T, sites[s][0], dtype, dev) for s in sites]
+        h = U.rand_act(rng, T, d, dtype, dev)
+        apply_lora_group_(ys, x, meta, pool, 0, tuple(sites))
+        apply_lora_group_tp_(ys, x, meta, pool, 0, tuple(sites), workspace=SplitWorkspace(meta, pool))
+        apply_reft_(h, meta, pool, 0)
+        torch.cuda.synchronize()
+        print("ok", dtype, lr, rr)
+
+
+if __name__ == "__main__":
+    main()
