@@ -182,17 +182,32 @@ constexpr int kSpAcc = 4;                 // split shrink accumulators = UMMA-is
 constexpr int kShrinkThreads = 32 * (6 + kSpAcc);
 
 struct SplitMaps {
-    CUtensorMap x;     // x [rows][m] (this rank's columns), 16-row x 64-col boxes
-    CUtensorMap A[3];  // A_s [S*R][m], R-row x 64-col boxes
-    CUtensorMap y[3];  // y_s [rows][n], 16-row x 64-col boxes
+    CUtensorMap x;       // x [rows][m] (this rank's columns), 16-row x 64-col boxes
+    CUtensorMap x64;     // the same with 64-row boxes (a unit of 4 contiguous chunks)
+    CUtensorMap A[3];    // A_s [S*R][m], R-row x 64-col boxes
+    CUtensorMap y[3];    // y_s [rows][n], 16-row x 64-col boxes
+    CUtensorMap y64[3];  // the same with 64-row boxes
 };
+
+// A unit whose 4 chunks are consecutive rows of one entry loads as ONE 64-row
+// TMA box: a TMA instruction costs ~100 cycles to issue, so per-chunk boxes
+// (4 per panel) capped the shrink at ~8 KB per 400 cycles per SM.
+__device__ __forceinline__ bool unit_contiguous(const int2* chunks, int4 U) {
+    if (U.z != 4) return false;
+    const int2 c0 = chunks[U.y], c1 = chunks[U.y + 1], c2 = chunks[U.y + 2], c3 = chunks[U.y + 3];
+    return c0.y == kSpChunk && c1.y == kSpChunk && c2.y == kSpChunk && c1.x == c0.x + kSpChunk &&
+           c2.x == c0.x + 2 * kSpChunk && c3.x == c0.x + 3 * kSpChunk;
+}
+
+constexpr int kPps = 4;  // K panels (64 columns each) per shrink ring stage: amortises the per-stage overheads
 
 template <int R, int NS>
 struct ShrinkLayout {
     static constexpr int NSR = NS * R;
-    static constexpr int X_BYTES = kSpU * 128;
+    static constexpr int PANEL = kSpU * 128;               // 64 rows x 64 columns
+    static constexpr int X_BYTES = kPps * PANEL;
     static constexpr int AP_BYTES = R * 128;
-    static constexpr int STAGE = X_BYTES + NS * AP_BYTES;  // multiple of 1024
+    static constexpr int STAGE = X_BYTES + kPps * NS * AP_BYTES;  // multiple of 1024
     static constexpr int STAGES_FIT = (227 * 1024 - 2048) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 16 ? 16 : STAGES_FIT;
     static constexpr int SMEM = STAGES * STAGE + 1024;
@@ -247,8 +262,9 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
             const int nch = U.z;
             const int row = lane < nch ? a.chunks[U.y + lane].x : 0;
-            const uint32_t bytes = static_cast<uint32_t>(nch * kSpChunk * 128 + NS * L::AP_BYTES);
-            for (int p = p0; p < p1; ++p) {
+            const bool contig = unit_contiguous(a.chunks, U);
+            const uint32_t bytes = static_cast<uint32_t>(kPps * (nch * kSpChunk * 128 + NS * L::AP_BYTES));
+            for (int p = p0; p < p1; p += kPps) {
                 if (lane == 0) {
                     tc::mbar_wait(&empty[stage], phase ^ 1u);
                     if (a.prof && blockIdx.x == 0 && npf < 128) a.prof[npf * 4 + 0] = clock64();
@@ -256,7 +272,17 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
                 }
                 __syncwarp();
                 const uint32_t st = sbase + stage * L::STAGE;
-                if (lane < nch) tc::tma_load_2d_hint(st + lane * (kSpChunk * 128), &maps.x, p * 64, row, &full[stage], stream);
+                const int rq = __shfl_sync(0xffffffffu, row, lane & 3);  // chunk (lane & 3)'s first row, all lanes
+                const int r0 = __shfl_sync(0xffffffffu, row, 0);         // the unit's first row
+                if (contig) {
+                    if (lane < kPps)
+                        tc::tma_load_2d_hint(st + lane * L::PANEL, &maps.x64, (p + lane) * 64, r0, &full[stage], stream);
+                } else if (lane < 4 * kPps) {
+                    const int pp = lane >> 2, q = lane & 3;
+                    if (q < nch)
+                        tc::tma_load_2d_hint(st + pp * L::PANEL + q * (kSpChunk * 128), &maps.x, (p + pp) * 64, rq,
+                                             &full[stage], stream);
+                }
                 ++npf;
                 if (++stage == L::STAGES) {
                     stage = 0;
@@ -274,12 +300,15 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
                 const int4 U = a.units[w / ks];
                 if (U.x >= a.slot_base) continue;
                 const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
-                for (int p = p0; p < p1; ++p) {
+                for (int p = p0; p < p1; p += kPps) {
                     tc::mbar_wait(&empty[stage], phase ^ 1u);
                     const uint32_t st = sbase + stage * L::STAGE;
 #pragma unroll
-                    for (int s = 0; s < NS; ++s)
-                        tc::tma_load_2d(st + L::X_BYTES + s * L::AP_BYTES, &maps.A[s], p * 64, U.x * R, &full[stage]);
+                    for (int pp = 0; pp < kPps; ++pp)
+#pragma unroll
+                        for (int s = 0; s < NS; ++s)
+                            tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s], (p + pp) * 64,
+                                            U.x * R, &full[stage]);
                     if (++stage == L::STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -305,17 +334,18 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
                 tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
                 tc::fence_after_sync();
                 const uint32_t dS = tmem + sb * kSpAcc * L::NSR;
-                for (int p = p0; p < p1; ++p) {
+                for (int p = p0; p < p1; p += kPps) {
                     tc::mbar_wait(&full[stage], phase);
                     if (a.prof && blockIdx.x == 0 && mw == 0 && nmc < 128) a.prof[nmc * 4 + 1] = clock64();
                     ++nmc;
                     tc::fence_after_sync();
                     const uint32_t st = sbase + stage * L::STAGE;
 #pragma unroll
-                    for (int k = mw; k < 4; k += kSpAcc) {
-                        const int kk = (p - p0) * 4 + k;
-                        tc::mma_bf16(dS + mw * L::NSR, tc::desc_kmajor_sw128(st + k * 32),
-                                     tc::desc_kmajor_sw128(st + L::X_BYTES + k * 32), id, kk >= kSpAcc ? 1u : 0u);
+                    for (int k = mw; k < 4 * kPps; k += kSpAcc) {
+                        const int kk = (p - p0) * 4 + k, pp = k >> 2, kq = k & 3;
+                        tc::mma_bf16(dS + mw * L::NSR, tc::desc_kmajor_sw128(st + pp * L::PANEL + kq * 32),
+                                     tc::desc_kmajor_sw128(st + L::X_BYTES + pp * NS * L::AP_BYTES + kq * 32), id,
+                                     kk >= kSpAcc ? 1u : 0u);
                     }
                     tc::mma_commit(&empty[stage]);
                     if (++stage == L::STAGES) {
@@ -465,6 +495,8 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
             if (U.x >= a.slot_base) continue;
             const int nch = U.z;
             const int row = q < nch ? a.chunks[U.y + q].x : 0;
+            const int row0 = a.chunks[U.y].x;
+            const bool contig = unit_contiguous(a.chunks, U);
             const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
             for (int c = c0; c < c1; ++c) {
                 int s, j;
@@ -477,10 +509,15 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                 }
                 __syncwarp();
                 const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
-                if (lane < 16 && pp < cw / 64 && q < nch)
+                if (contig) {
+                    if (lane < cw / 64)  // one 64-row box per panel
+                        tc::tma_load_2d_hint(st + lane * kSpU * 128, &maps.y64[s], j * cw + lane * 64, row0, &full[stage],
+                                             stream);
+                } else if (lane < 16 && pp < cw / 64 && q < nch) {
                     tc::tma_load_2d_hint(st + pp * kSpU * 128 + q * (kSpChunk * 128), &maps.y[s], j * cw + pp * 64, row,
                                          &full[stage], stream);
-                else if (lane == 16)
+                }
+                if (lane == 16)
                     tc::bulk_load_1d(st + L::Y_BYTES,
                                      static_cast<const unsigned char*>(a.site[s].Bt_tc) +
                                          static_cast<long long>(U.x) * a.site[s].n * R * 2 +
@@ -793,14 +830,16 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
     args.m = m;
     fill_common(args, meta, sites, nsites, P, ldp);
     const int variant = split_variant();
-    bool tc_ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && m % 64 == 0 && ldx % 8 == 0 && ldp % 4 == 0 &&
+    bool tc_ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && m % (64 * kPps) == 0 && ldx % 8 == 0 && ldp % 4 == 0 &&
                  al16(x) && al16(P) && meta->chunks && meta->units;
     for (int s = 0; s < nsites; ++s) tc_ok = tc_ok && al16(sites[s].A);
     if (variant == 1 && !tc_ok) return PREFT_ERR_SHAPE;
     if (variant != 0 && tc_ok) {
         SplitMaps maps{};
         if (!make_tmap_bf16_sw128(&maps.x, x, static_cast<unsigned long long>(rows), static_cast<unsigned long long>(m),
-                                  static_cast<unsigned long long>(ldx), 64, kSpChunk))
+                                  static_cast<unsigned long long>(ldx), 64, kSpChunk) ||
+            !make_tmap_bf16_sw128(&maps.x64, x, static_cast<unsigned long long>(rows), static_cast<unsigned long long>(m),
+                                  static_cast<unsigned long long>(ldx), 64, kSpU))
             return PREFT_ERR_CONFIG;
         for (int s = 0; s < nsites; ++s)
             if (!make_tmap_bf16_sw128(&maps.A[s], sites[s].A, 1ull << 20, static_cast<unsigned long long>(m),
@@ -857,7 +896,10 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
         for (int s = 0; s < nsites; ++s)
             if (!make_tmap_bf16_sw128(&maps.y[s], sites[s].y, static_cast<unsigned long long>(rows),
                                       static_cast<unsigned long long>(sites[s].n),
-                                      static_cast<unsigned long long>(sites[s].ldy), 64, kSpChunk))
+                                      static_cast<unsigned long long>(sites[s].ldy), 64, kSpChunk) ||
+                !make_tmap_bf16_sw128(&maps.y64[s], sites[s].y, static_cast<unsigned long long>(rows),
+                                      static_cast<unsigned long long>(sites[s].n),
+                                      static_cast<unsigned long long>(sites[s].ldy), 64, kSpU))
                 return PREFT_ERR_CONFIG;
         if (r == 16) {
             if (nsites == 1) return launch_tc(expand_tc_kernel<16, 1>, ExpandLayout<16, 1>::SMEM, 384, maps, args, num_sms, stream);

@@ -11,6 +11,8 @@ sys.path.insert(0, str(ROOT))
 
 
 def main():
+    import os
+
     import torch
 
     import bench
@@ -24,7 +26,13 @@ def main():
     pool = AdapterPool(1, shape.d_model, lora_sites=shape.site_dims(), lora_capacity=512, lora_rank=16,
                        dtype=torch.bfloat16, device=dev, tp_rank=0, tp_size=8)
     pool.fill_synthetic_(512, AdapterKind.LORA, 16, seed=1)
-    qsl, ids, flags, lens, _ = bench.step_entries(0, 1, 256, 256, seed=3)
+    if os.environ.get("LONG"):
+        lens = [2048] * 32
+        qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        ids = [int(i) * 7 % 512 for i in range(32)]
+        flags = np.zeros(32, np.int32)
+    else:
+        qsl, ids, flags, lens, _ = bench.step_entries(0, 1, 256, 256, seed=3)
     slots = pool.entry_arrays(qsl, ids, flags)
     T = int(qsl[-1])
     meta = BatchMeta(len(ids), T, device=dev)
@@ -32,8 +40,8 @@ def main():
     meta.build_arrays(qsl, slots, flags)
     print("units", meta.units_host().shape[0], "chunks", meta.chunks_host().shape[0], file=sys.stderr)
     ws = SplitWorkspace(meta, pool)
-    group = ("Wq", "Wk", "Wv")
-    x = torch.randn(T, 8192, device=dev).to(torch.bfloat16)
+    group = ("Wo",) if os.environ.get("LONG") else ("Wq", "Wk", "Wv")
+    x = torch.randn(T, pool.lora_shard[group[0]].x_width, device=dev).to(torch.bfloat16)
     ys = [torch.randn(T, pool.lora_shard[s].y_width, device=dev).to(torch.bfloat16) for s in group]
     lib = _lib.load()
     for _ in range(3):
@@ -46,7 +54,7 @@ def main():
     st = buf.view(128, 4).cpu().numpy()
     t0 = st[0, 0]
     print("stage: producer_issue mma_consume | unit: s_full")
-    for i in range(64):
+    for i in range(128):
         if st[i, 0] or st[i, 1] or st[i, 2]:
             print(i, *(int(v - t0) if v else 0 for v in st[i, :3]))
 
