@@ -26,6 +26,16 @@ int reft_tc_last_grid();
 void reft_tc_set_profile(long long* buf);
 void reft_tc_set_flags(int flags, int look);
 
+// programmatic dependent launch of the tensor-core kernels (PREFT_PDL=0 disables)
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("PREFT_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
 static thread_local char g_last_cuda_error[256] = "";
 
 static int record_cuda(cudaError_t e) {

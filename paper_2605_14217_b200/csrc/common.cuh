@@ -188,6 +188,14 @@ __device__ __forceinline__ A warp_sum(A v) {
     return v;
 }
 
+// Programmatic dependent launch (sm_90+): let the next kernel in the stream
+// launch now, then wait until the previous kernel's writes are visible.  Both
+// are no-ops when the kernel was launched without the PDL attribute.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // Contiguous share [lo, hi) of n items for worker w of nw (balanced to +-1).
 __device__ __forceinline__ void even_share(int n, int w, int nw, int& lo, int& hi) {
     lo = static_cast<int>((static_cast<long long>(w) * n) / nw);

@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) lora_kernel(const LoraArgs a) {
     const int lane = threadIdx.x & 31;
     const int gw = static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
     const int nw = static_cast<int>((gridDim.x * blockDim.x) >> 5);
+    pdl_begin();  // programmatic dependent launch: wait for the previous kernel's writes
     const int n_tok = a.counters[PREFT_CTR_SPLIT];  // LoRA-class tokens: sorted [0, split)
     int i0, i1;
     even_share(n_tok, gw, nw, i0, i1);
@@ -204,6 +205,7 @@ int lora_variant() {
 void set_lora_variant(int v) { g_lora_variant = v; }
 
 int grid_for(const void* fn, int threads, int num_sms);
+bool pdl_enabled();
 
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
                int nsites, int r, int dtype, cudaStream_t stream, int num_sms) {
@@ -259,7 +261,16 @@ int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, co
                                         : pick_lora<double>(vec, nsites, r);
     if (!fn) return PREFT_ERR_RANK;
     const int grid = grid_for(reinterpret_cast<const void*>(fn), 256, num_sms);
-    fn<<<grid, 256, 0, stream>>>(args);
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, fn, args);
     const cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? PREFT_OK : -static_cast<int>(e);
 }

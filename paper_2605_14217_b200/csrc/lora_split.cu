@@ -245,6 +245,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
     // work item = (unit, 1/ks of the K panels): ks = 2 balances launches with
     // ~2 units per SM; the two halves meet in P through f32 atomics, whose
     // order cannot change a two-term sum (0 + a + b == 0 + b + a)
+    tc::pdl_launch_dependents();
+    tc::pdl_wait();  // everything below reads the previous kernels' output
     const int ks = a.ks;
     int w0, w1;
     even_share(a.counters[PREFT_CTR_UNITS] * ks, blockIdx.x, gridDim.x, w0, w1);
@@ -481,6 +483,8 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tslot;
+    tc::pdl_launch_dependents();
+    tc::pdl_wait();  // everything below reads the previous kernels' output
     ExpandItems it;
     it.init(a, NS);
 
@@ -780,13 +784,24 @@ int split_variant() {
 }
 void set_split_variant(int v) { g_split_variant = v; }
 
+bool pdl_enabled();
+
 template <typename K>
 static int launch_tc(K kernel, int smem, int threads, const SplitMaps& maps, const SplitArgs& args, int num_sms,
                      cudaStream_t stream) {
     cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return -static_cast<int>(e);
-    kernel<<<num_sms, threads, smem, stream>>>(maps, args);
-    e = cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.gridDim = dim3(num_sms);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    e = cudaLaunchKernelEx(&cfg, kernel, maps, args);
     return e == cudaSuccess ? PREFT_OK : -static_cast<int>(e);
 }
 

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kTeamCtaThreads, MINB) lora_team_kernel(const 
     __shared__ acc_t vsh[TEAMS][NR];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int team = warp / TEAM, tt = threadIdx.x % TT;
+    pdl_begin();  // programmatic dependent launch: wait for the previous kernel's writes
     const int n_tok = a.counters[PREFT_CTR_SPLIT];
     int i0, i1;
     even_share(n_tok, blockIdx.x * TEAMS + team, gridDim.x * TEAMS, i0, i1);
