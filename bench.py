@@ -409,25 +409,32 @@ def punica_step(args, rank, world, device):
     return out
 
 
-def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, steps: int = 5) -> dict:
+def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, steps: int = 5,
+                world: int = 1, grank: int = 0) -> dict:
     """Secondary line: a ReFT^P residual site x 32 layers (8B shapes) over one
-    batch of long prompts, one fused launch per layer (BASELINE configs 3/5)."""
+    batch of long prompts, one fused launch per layer (BASELINE configs 3/5).
+    With `world` GPUs each rank holds its shard of the 512 adapters (adapter
+    a lives on GPU a mod world) and serves prompts routed to them (weak
+    scaling, no collective on the data path)."""
     import torch
 
     from paper_2605_14217_b200 import AdapterKind, shapes
     from paper_2605_14217_b200.meta import BatchMeta
     from paper_2605_14217_b200.plan import StepPlan
     from paper_2605_14217_b200.pool import AdapterPool
+    from paper_2605_14217_b200.workload import shard_adapters
 
     d = shapes.LLAMA_8B.d_model
     kind = AdapterKind(kind_name)
-    pool = AdapterPool(N_LAYERS, d, reft_capacity=N_ADAPTERS, reft_rank=rank, dtype=torch.bfloat16, device=device)
-    pool.fill_synthetic_(N_ADAPTERS, kind, rank, seed=5)
+    owned = shard_adapters(N_ADAPTERS, grank, world)
+    ids = [int(owned[int(a) % len(owned)]) for a in ids]  # requests routed to this GPU's adapters
+    pool = AdapterPool(N_LAYERS, d, reft_capacity=len(owned), reft_rank=rank, dtype=torch.bfloat16, device=device)
+    pool.fill_synthetic_(0, kind, rank, seed=5 + grank, ids=owned)
     n_dec = 64
     all_lens = np.concatenate([np.ones(n_dec, dtype=np.int64), np.asarray(lens, dtype=np.int64)])
     qsl = np.concatenate([[0], np.cumsum(all_lens)]).astype(np.int32)
     flags = np.array([1] * n_dec + [0] * len(lens), dtype=np.int32)
-    eids = [int(i) % N_ADAPTERS for i in range(n_dec)] + [int(a) for a in ids]
+    eids = [int(owned[i % len(owned)]) for i in range(n_dec)] + [int(a) for a in ids]
     slots = pool.entry_arrays(qsl, eids, flags)
     T = int(qsl[-1])
     meta = BatchMeta(len(eids), T, tile_tokens=128, device=device)
@@ -442,22 +449,26 @@ def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, 
         plan.run(s)
     plan.set_timing(1, steps * N_LAYERS)
     torch.cuda.synchronize()
+    barrier(world)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
     for _ in range(steps):
         plan.run(s)
     e1.record(s)
     torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+    ms = all_max(e0.elapsed_time(e1) / steps, world)
     k_ms, k_n = plan.collect_timing()
     sel = int(np.sum(lens))
+    sel_all = int(all_sum(sel, world))
     distinct = len(set(int(a) for a in ids))
     per_launch = sel * 2 * d * 2 + distinct * 2 * (2 * rank * d) + distinct * 4 * rank
     peak, _ = measured_peak_gbs()
     frac = per_launch / (k_ms / k_n / 1e3) / 1e9 / peak
-    out = {"workload": label, "prefill_tokens": sel, "ms_per_step": round(ms, 3),
-           "value": round(sel / (ms / 1e3), 1), "unit": UNIT, "kernel_frac_of_hbm_peak": round(frac, 4),
-           "avg_launch_us": round(k_ms / k_n * 1e3, 2)}
+    frac = all_sum(frac, world) / world
+    out = {"workload": label + (f" [{world} GPUs, adapter-sharded, weak scaling]" if world > 1 else ""),
+           "prefill_tokens": sel_all, "ms_per_step": round(ms, 3),
+           "value": round(sel_all / (ms / 1e3), 1), "unit": UNIT, "kernel_frac_of_hbm_peak": round(frac, 4),
+           "avg_launch_us": round(k_ms / k_n * 1e3, 2), "n_gpus": world}
     del pool, meta, plan, h
     torch.cuda.empty_cache()
     return out
@@ -709,20 +720,22 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
     return out
 
 
-def secondary_configs(args, device) -> list:
+def secondary_configs(args, device, world: int = 1, rank: int = 0) -> list:
     from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig, assign_adapters
 
-    out = [lora_reft_mix_config(args, device)]
+    out = [lora_reft_mix_config(args, device)] if world == 1 else []
     rng = np.random.default_rng(3)
     ids3 = rng.integers(0, N_ADAPTERS, size=32)
     out.append(reft_config(args, device, "direft", 16, [2048] * 32, ids3,
-                           "cfg3 slice (1 GPU): 8B shapes, DiReFT^P r16 x 32 layers, 512 adapters, 32 x 2048-token "
-                           "prompts + 64 decode"))
+                           "cfg3: 8B shapes, DiReFT^P r16 x 32 layers, 512 adapters, 32 x 2048-token prompts + 64 decode "
+                           "per GPU", world=world, grank=rank))
     ids5 = assign_adapters(WorkloadConfig(8, N_ADAPTERS, AdapterMix.SKEWED, seed=5))
     lens5 = rng.integers(8192, 16385, size=8)
     out.append(reft_config(args, device, "loreft", 32, lens5, ids5,
-                           "cfg5 slice (1 GPU): Zipf over 512 adapters, 8 prompts U[8k,16k], LoReFT^P r32 x 32 layers"))
-    out.append(serving_replay(args, device))
+                           "cfg5: Zipf over 512 adapters, 8 prompts U[8k,16k] per GPU, LoReFT^P r32 x 32 layers",
+                           world=world, grank=rank))
+    if world == 1:
+        out.append(serving_replay(args, device))
     return out
 
 
@@ -779,10 +792,10 @@ def run_ours(args):
     if not args.no_punica_step and world == 1:
         punica = punica_step(args, rank, world, device)
     others = None
-    if not args.no_secondary and world in (1, 8):
+    if not args.no_secondary:
         del ctx["plan"], ctx["acts"]
         torch.cuda.empty_cache()
-        others = secondary_configs(args, device) if world == 1 else []
+        others = secondary_configs(args, device, world, rank)
         try:
             cfg4 = tp_config(args, device, world, rank)
         except Exception as exc:  # never lose the headline line to the secondary config
