@@ -51,13 +51,16 @@ constexpr int kEpiN = 128;                // expand / epilogue chunk width (UMMA
 constexpr int kTcThreads = 512;           // 16 warps
 constexpr int kNacc = 2;                  // split shrink accumulators
 constexpr int kEpiWarps = 8;
-constexpr int kSPps = 2;  // K panels per shrink ring stage (amortises the per-stage issue and barrier costs)
+// K panels per shrink ring stage: issuing several panels of the same rows
+// together amortises the per-stage costs and gives DRAM longer runs per row
+constexpr int spps_for(int R, int C) { return R == 16 && C == 2 ? 4 : 2; }
 
 template <int R, int C>
 struct TcLayout {
     static constexpr int H_BYTES = kUnitRows * 128;      // 64 rows x 64 bf16 (one 128 B-swizzled panel)
     static constexpr int AP_BYTES = R * 128;             // A panel: R rows x 64 bf16
-    static constexpr int SH_STAGE = kSPps * (H_BYTES + AP_BYTES);  // kSPps panels of h, then their A panels
+    static constexpr int SPPS = spps_for(R, C);
+    static constexpr int SH_STAGE = SPPS * (H_BYTES + AP_BYTES);  // SPPS panels of h, then their A panels
     static constexpr int EH_BYTES = 2 * H_BYTES;         // 128 columns = two panels
     static constexpr int BT_BYTES = kEpiN * R * 2;       // Bt chunk: 128 rows x R (core-matrix layout)
     static constexpr int EPI_STAGE = EH_BYTES + BT_BYTES;
@@ -289,9 +292,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0 && ub > 0 && !(a.flags & 4)) tc::mbar_wait(&v_full[(ub - 1) & 1], ((ub - 1) >> 1) & 1);
             ++ub;
             const int row = lane < nch ? a.chunks[U.y + lane].x : 0;
-            const uint32_t bytes = static_cast<uint32_t>(kSPps * (nch * kChunk * 128 + L::AP_BYTES));
+            const uint32_t bytes = static_cast<uint32_t>(L::SPPS * (nch * kChunk * 128 + L::AP_BYTES));
             const int rq = __shfl_sync(0xffffffffu, row, lane & 3);
-            for (int p = 0; p < NP; p += kSPps) {
+            for (int p = 0; p < NP; p += L::SPPS) {
                 if (lane == 0) {
                     tc::mbar_wait(&sh_empty[stage], phase ^ 1u);
                     if ((a.flags & 2) && ub > 1) {
@@ -304,12 +307,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 __syncwarp();
                 const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
                 const int pp = lane >> 2, q = lane & 3;  // lane 4*pp + q: panel pp of chunk q; lanes 16+: A panels
-                if (lane < 4 * kSPps) {
+                if (lane < 4 * L::SPPS) {
                     if (q < nch)
                         tc::tma_load_2d_hint(st + pp * L::H_BYTES + q * (kChunk * 128), &tmH, (pc0 + p + pp) * 64, rq,
                                              &sh_full[stage], keep);
-                } else if (lane >= 16 && lane < 16 + kSPps) {
-                    tc::tma_load_2d(st + kSPps * L::H_BYTES + (lane - 16) * L::AP_BYTES, &tmA, (pc0 + p + lane - 16) * 64,
+                } else if (lane >= 16 && lane < 16 + L::SPPS) {
+                    tc::tma_load_2d(st + L::SPPS * L::H_BYTES + (lane - 16) * L::AP_BYTES, &tmA, (pc0 + p + lane - 16) * 64,
                                     slot * R, &sh_full[stage]);
                 }
                 if (++stage == L::SH_STAGES) {
@@ -331,19 +334,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
                 tc::fence_after_sync();
                 const uint32_t dS = tmem + sb * L::S_COLS;
-                for (int p = 0; p < NP; p += kSPps) {
+                for (int p = 0; p < NP; p += L::SPPS) {
                     tc::mbar_wait(&sh_full[stage], phase);
                     // these rows are in L2 now: the epilogue producer may re-read them
-                    atomicMax(&s_shrunk, (ub * NP) + p + kSPps);  // shared-memory atomics: an explicit, race-free flag
-                    if (a.prof && blockIdx.x == 0 && ub < 16 && (p == 0 || p + kSPps >= NP))
+                    atomicMax(&s_shrunk, (ub * NP) + p + L::SPPS);  // shared-memory atomics: an explicit, race-free flag
+                    if (a.prof && blockIdx.x == 0 && ub < 16 && (p == 0 || p + L::SPPS >= NP))
                         a.prof[576 + ub * 2 + (p ? 1 : 0)] = clock64();
                     tc::fence_after_sync();
                     const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
 #pragma unroll
-                    for (int k = 0; k < 4 * kSPps; ++k) {
+                    for (int k = 0; k < 4 * L::SPPS; ++k) {
                         const int kk = p * 4 + k, pp = k >> 2, kq = k & 3;
                         tc::mma_bf16(dS + (kk % kNacc) * R, tc::desc_kmajor_sw128(st + pp * L::H_BYTES + kq * 32),
-                                     tc::desc_kmajor_sw128(st + kSPps * L::H_BYTES + pp * L::AP_BYTES + kq * 32), id,
+                                     tc::desc_kmajor_sw128(st + L::SPPS * L::H_BYTES + pp * L::AP_BYTES + kq * 32), id,
                                      kk >= kNacc ? 1u : 0u);
                     }
                     tc::mma_commit(&sh_empty[stage]);
@@ -635,7 +638,7 @@ static int tc_cluster_for(int d) {
 int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A,
                   const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms) {
     if (!Bt || (r != 16 && r != 32) || d < 128 || d % 128 || rows < 1) return PREFT_ERR_SHAPE;
-    if ((d / tc_cluster_for(d)) % (64 * kSPps)) return PREFT_ERR_SHAPE;
+    if ((d / tc_cluster_for(d)) % (64 * spps_for(r, tc_cluster_for(d)))) return PREFT_ERR_SHAPE;
     if (!meta->chunks || !meta->units || (ldh % 8) || (reinterpret_cast<uintptr_t>(h) & 15) ||
         (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(Bt) & 15))
         return PREFT_ERR_SHAPE;
