@@ -302,7 +302,7 @@ int preft_tc_selftest(const void* A, const void* B, float* D, int32_t K, int32_t
 
 /* Diagnostic: route clock64() stamps of the tensor-core ReFT kernel's CTA 0
  * (8 per chunk for 64 chunks, 4 per unit and 2 shrink stamps per unit for 16
- * units; device buffer of >= 608 int64, NULL = off) and return the grid size of the last launch. */
+ * units; device buffer of >= 736 int64, NULL = off) and return the grid size of the last launch. */
 int preft_diag_reft_tc(long long* device_buffer);
 
 /* library / device introspection */

@@ -102,14 +102,17 @@ struct ReftTcArgs {
                 // epilogue producer read ahead of the shrink, bit 4 no L2 hints, bit 5
                 // reduce epilogue (bf16 delta added into h by TMA in L2, no re-read)
     int look;   // with bit 1: panels the shrink may run ahead of the epilogue's re-read
-    long long* prof;  // diagnostics: clock64 stamps of CTA 0 (NULL in production)
+    long long* prof;  // diagnostics: clock64 stamps of CTA prof_cta (NULL in production)
+    int prof_cta;
 };
 
 // diagnostics: warp 4 lane 0 of CTA 0 stamps chunk phases (first 64 chunks) and unit phases
 #define PROF(k) \
-    if (a.prof && blockIdx.x == 0 && warp == 4 && lane == 0 && dc < 64) a.prof[dc * 8 + (k)] = clock64()
+    if (a.prof && blockIdx.x == a.prof_cta && warp == 4 && lane == 0 && dc < 64) a.prof[dc * 8 + (k)] = clock64()
+#define XPROF(k, v) \
+    if (a.prof && blockIdx.x == a.prof_cta && warp == 12 && lane == 0 && ub < 16) a.prof[608 + ub * 8 + (k)] = (v)
 #define UPROF(k) \
-    if (a.prof && blockIdx.x == 0 && warp == 12 && lane == 0 && ub < 16) a.prof[512 + ub * 4 + (k)] = clock64()
+    if (a.prof && blockIdx.x == a.prof_cta && warp == 12 && lane == 0 && ub < 16) a.prof[512 + ub * 4 + (k)] = clock64()
 
 template <int R, int C>
 __global__ void __launch_bounds__(kTcThreads, 1)
@@ -149,8 +152,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::mbar_init(&v_empty[b], 1);
             tc::mbar_init(&d_full[b], 1);
             tc::mbar_init(&d_empty[b], kEpiWarps);
-            tc::mbar_init(&p_full[b], 128 * (C - 1));   // every lane of 4 warps of each peer
-            tc::mbar_init(&p_empty[b], 128 * (C - 1));
+            tc::mbar_init(&p_full[b], 4);             // the 4 local V warps (expect_tx of the peers' st.async bytes)
+            tc::mbar_init(&p_empty[b], 4 * (C - 1));  // the 4 V warps of each peer
         }
         tc::fence_mbar_init();
         tc::prefetch_tmap(&tmH);
@@ -211,20 +214,27 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 // S is a partial sum over this CTA's columns: push it to every
                 // peer's inbox, then add the peers' partials from our own
                 const int m = q * kChunk + (lane & 15);
-                tc::mbar_wait_cluster(&p_empty[sb], ((ub >> 1) & 1) ^ 1u);  // peers done with unit u-2
+                // every peer's st.async completes its bytes on our p_full: expect them
+                if (lane == 0) tc::mbar_expect_tx(&p_full[sb], (C - 1) * kChunk * R * 4);
+                tc::mbar_wait(&p_empty[sb], ((ub >> 1) & 1) ^ 1u);  // peers done with unit u-2 (flow control only)
+                XPROF(0, clock64());
+                XPROF(4, static_cast<long long>(tc::globaltimer()));
 #pragma unroll
                 for (int x = 1; x < C; ++x) {
                     const int peer = (crank + x) % C;  // our slot in peer's inbox: C - 1 - x
                     const uint32_t dst = tc::map_shared(
                         sbase + L::OFF_IN + (sb * (C - 1) + (C - 1 - x)) * L::IN_BYTES + m * R * 4, peer);
+                    const uint32_t bar = tc::map_shared(tc::smem_u32(&p_full[sb]), peer);
                     if (lane < kChunk) {
 #pragma unroll
                         for (int k = 0; k < R; k += 4)
-                            tc::st_dsmem_f4(dst + k * 4, make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]));
+                            tc::st_async_f4(dst + k * 4, make_float4(s[k], s[k + 1], s[k + 2], s[k + 3]), bar);
                     }
-                    tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_full[sb]), peer));
                 }
-                tc::mbar_wait_cluster(&p_full[sb], (ub >> 1) & 1);
+                XPROF(1, clock64());
+                tc::mbar_wait(&p_full[sb], (ub >> 1) & 1);
+                XPROF(2, clock64());
+                XPROF(5, static_cast<long long>(tc::globaltimer()));
                 if (lane < kChunk) {
 #pragma unroll
                     for (int x = 0; x < C - 1; ++x) {
@@ -240,9 +250,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                         }
                     }
                 }
-#pragma unroll
-                for (int x = 1; x < C; ++x)
-                    tc::mbar_arrive_remote(tc::map_shared(tc::smem_u32(&p_empty[sb]), (crank + x) % C));
             }
             tc::mbar_wait(&v_empty[sb], ((ub >> 1) & 1) ^ 1u);
             UPROF(2);
@@ -270,7 +277,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
             tc::fence_proxy_async();  // V (generic writes) -> tensor-core operand reads
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&v_full[sb]);
+            if (lane == 0) {
+                tc::mbar_arrive(&v_full[sb]);
+                // the inbox was consumed into V (written above, in issue order after the
+                // inbox loads returned): the peers may overwrite it with unit u+2
+                if constexpr (C > 1) {
+#pragma unroll
+                    for (int x = 1; x < C; ++x)
+                        tc::mbar_arrive_remote_relaxed(tc::map_shared(tc::smem_u32(&p_empty[sb]), (crank + x) % C));
+                }
+            }
             UPROF(3);
         
             ++ub;
@@ -338,7 +354,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     tc::mbar_wait(&sh_full[stage], phase);
                     // these rows are in L2 now: the epilogue producer may re-read them
                     atomicMax(&s_shrunk, (ub * NP) + p + L::SPPS);  // shared-memory atomics: an explicit, race-free flag
-                    if (a.prof && blockIdx.x == 0 && ub < 16 && (p == 0 || p + L::SPPS >= NP))
+                    if (a.prof && blockIdx.x == a.prof_cta && ub < 16 && (p == 0 || p + L::SPPS >= NP))
                         a.prof[576 + ub * 2 + (p ? 1 : 0)] = clock64();
                     tc::fence_after_sync();
                     const uint32_t st = sbase + L::OFF_SH + stage * L::SH_STAGE;
@@ -417,10 +433,10 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                 const uint32_t vhi = sbase + L::OFF_V + vb * 2 * L::V_BYTES, vlo = vhi + L::V_BYTES;
                 for (int j = 0; j < NJ; ++j) {
                     tc::mbar_wait(&epi_full[stage], phase);
-                    if (a.prof && blockIdx.x == 0 && dc < 64) a.prof[dc * 8 + 0] = clock64();
+                    if (a.prof && blockIdx.x == a.prof_cta && dc < 64) a.prof[dc * 8 + 0] = clock64();
                     const int db = dc & 1;
                     tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
-                    if (a.prof && blockIdx.x == 0 && dc < 64) a.prof[dc * 8 + 1] = clock64();
+                    if (a.prof && blockIdx.x == a.prof_cta && dc < 64) a.prof[dc * 8 + 1] = clock64();
                     tc::fence_after_sync();
                     const uint32_t bt = sbase + L::OFF_EPI + stage * L::EPI_STAGE + L::EH_BYTES;
                     const uint32_t dD = tmem + L::D_COL0 + db * kEpiN;
@@ -432,7 +448,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
                     }
                     tc::mma_commit(&d_full[db]);
                     tc::mma_commit(&epi_empty[stage]);  // Bt chunk no longer read
-                    if (a.prof && blockIdx.x == 0 && dc < 64) a.prof[dc * 8 + 2] = clock64();
+                    if (a.prof && blockIdx.x == a.prof_cta && dc < 64) a.prof[dc * 8 + 2] = clock64();
                     if (++stage == L::EPI_STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -675,6 +691,8 @@ int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long l
         // the shrink may run 3/4 of a unit ahead of the epilogue's re-read
         args.look = look >= 0 ? look : (d / 64) / tc_cluster_for(d) * 3 / 4;
         args.prof = g_tc_prof;
+        const char* pc = g_tc_prof ? getenv("PREFT_REFT_PROF_CTA") : nullptr;
+        args.prof_cta = pc ? atoi(pc) : 0;
     }
     const int c = tc_cluster_for(d);
     if (r == 16)

@@ -166,6 +166,11 @@ __device__ __forceinline__ void prefetch_tmap(const void* tmap) {
 }
 
 // ---- L2 cache-policy hints (createpolicy) for TMA traffic
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -284,6 +289,21 @@ __device__ __forceinline__ void st_dsmem_f4(uint32_t addr, float4 v) {
 // releasing this thread's prior writes at cluster scope
 __device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
     asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+// asynchronous 16-byte store into another CTA's shared memory that completes
+// its bytes on an mbarrier of that CTA (no fence: the barrier carries them)
+__device__ __forceinline__ void st_async_f4(uint32_t cluster_addr, float4 v, uint32_t cluster_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.f32 [%0], {%1,%2,%3,%4}, [%5];" ::"r"(
+                     cluster_addr),
+                 "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w), "r"(cluster_mbar)
+                 : "memory");
+}
+
+// relaxed remote arrive: a flow-control signal that orders no memory (a
+// release at cluster scope costs a MEMBAR.GPU per arriving thread)
+__device__ __forceinline__ void mbar_arrive_remote_relaxed(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
 }
 
 // wait for a phase of a local mbarrier whose arrivals come from other CTAs of the cluster

@@ -61,7 +61,7 @@ def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False):
     if prof and variant == 1:
         import ctypes
 
-        buf = torch.zeros(608, dtype=torch.int64, device=dev)
+        buf = torch.zeros(736, dtype=torch.int64, device=dev)
         lib.preft_set_reft_variant(1)
         lib.preft_diag_reft_tc(ctypes.c_void_p(buf.data_ptr()))
         apply_reft_(hs[0], meta, pool, 0)
@@ -72,16 +72,19 @@ def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False):
         ch = st[:512].reshape(64, 8).astype(np.int64)
         un = st[512:576].reshape(16, 4).astype(np.int64)
         sh = st[576:608].reshape(16, 2).astype(np.int64)
+        xp = st[608:736].reshape(16, 8).astype(np.int64)
         t0 = int(un[0, 0])
         names = ["mma_epi_full", "mma_d_empty", "mma_issued", "ep_d_full", "ep_epi_full", "ep_ldtm", "ep_rmw", "ep_released"]
         print("chunk timeline (cycles from unit 0 s_full), " + " ".join(names), file=sys.stderr)
-        for c in range(min(40, len(ch))):
+        for c in range(len(ch)):
             print(c, " ".join(f"{int(v) - t0:8d}" for v in ch[c]), file=sys.stderr)
         print("units: s_full, S loaded, exchanged, v_full | shrink first panel, last panel", file=sys.stderr)
         for u in range(16):
             if un[u, 0]:
                 print(u, " ".join(f"{int(v) - t0:8d}" for v in un[u]), "|",
-                      " ".join(f"{int(v) - t0:8d}" for v in sh[u]), file=sys.stderr)
+                      " ".join(f"{int(v) - t0:8d}" for v in sh[u]), "| p_empty ok, pushed, p_full ok",
+                      " ".join(f"{int(v) - t0:8d}" for v in xp[u, :3]), "| gt", int(xp[u, 4]), int(xp[u, 5]),
+                      file=sys.stderr)
     distinct = len(set(int(i) for i in ids))
     alg = T * 2 * d * 2 + distinct * 2 * (2 * rank * d) + distinct * 4 * rank
     gbs = alg / us / 1e3
