@@ -240,7 +240,9 @@ int preft_reft_apply(const preft_meta_t* meta, void* h, int64_t rows, int64_t ld
                      const void* scale, int32_t r_max, int32_t dtype, void* stream);
 
 /* K3 kernel variant: -1 automatic (default), 0 SIMT only, 1 tensor cores
- * only (PREFT_ERR_SHAPE when ineligible).  Env: PREFT_REFT_VARIANT=simt|tc. */
+ * only (resident kernel when eligible, else streaming; PREFT_ERR_SHAPE when
+ * neither applies), 2 streaming tensor-core kernel only, 3 resident
+ * tensor-core kernel only.  Env: PREFT_REFT_VARIANT=simt|tc|pass|res. */
 int preft_set_reft_variant(int32_t variant);
 
 /* Tensor-core ReFT pipeline knobs (diagnostics / A-B measurement; results

@@ -219,7 +219,7 @@ int preft_set_reft_tc_flags(int32_t flags, int32_t look) {
 }
 
 int preft_set_reft_variant(int32_t variant) {
-    if (variant < -1 || variant > 1) return PREFT_ERR_DOMAIN;
+    if (variant < -1 || variant > 3) return PREFT_ERR_DOMAIN;
     set_reft_variant(variant);
     return PREFT_OK;
 }

@@ -183,13 +183,18 @@ int grid_for(const void* fn, int threads, int num_sms);
 
 int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A, const void* Bt,
                   const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms);
+int reft_res_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A,
+                   const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms);
+bool reft_res_preferred(int d, int r);
 
 // -1 automatic (tensor cores when eligible), 0 SIMT only, 1 tensor cores only
+// (resident kernel when eligible, else streaming), 2 streaming tensor-core
+// kernel only, 3 resident tensor-core kernel only
 static int g_reft_variant = -2;
 int reft_variant() {
     if (g_reft_variant == -2) {
         const char* env = getenv("PREFT_REFT_VARIANT");
-        g_reft_variant = (env && env[0] == 's') ? 0 : (env && env[0] == 't') ? 1 : -1;
+        g_reft_variant = !env ? -1 : env[0] == 's' ? 0 : env[0] == 't' ? 1 : env[0] == 'p' ? 2 : env[0] == 'r' ? 3 : -1;
     }
     return g_reft_variant;
 }
@@ -203,9 +208,13 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
     if (dtype != PREFT_DTYPE_F32 && dtype != PREFT_DTYPE_BF16 && dtype != PREFT_DTYPE_F64) return PREFT_ERR_DOMAIN;
     const int variant = reft_variant();
     if (variant != 0 && Bt && dtype == PREFT_DTYPE_BF16) {
-        const int rc = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms);
-        if (rc != PREFT_ERR_SHAPE || variant == 1) return rc;  // launched, failed, or TC forced
-    } else if (variant == 1) {
+        int rc = PREFT_ERR_SHAPE;
+        if (variant == 3 || (variant != 2 && reft_res_preferred(d, r)))
+            rc = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms);
+        if (rc != PREFT_ERR_SHAPE || variant == 3) return rc;  // launched, failed, or resident forced
+        rc = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms);
+        if (rc != PREFT_ERR_SHAPE || variant >= 1) return rc;  // launched, failed, or TC forced
+    } else if (variant >= 1) {
         return PREFT_ERR_SHAPE;
     }
     const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;

@@ -108,7 +108,7 @@ struct ReftTcArgs {
 
 // diagnostics: warp 4 lane 0 of CTA 0 stamps chunk phases (first 64 chunks) and unit phases
 #define PROF(k) \
-    if (a.prof && blockIdx.x == a.prof_cta && warp == 4 && lane == 0 && dc < 64) a.prof[dc * 8 + (k)] = clock64()
+    if (a.prof && blockIdx.x == a.prof_cta && (warp == 4 || warp == 8) && lane == 0 && dc < 64) a.prof[dc * 8 + (k)] = clock64()
 #define XPROF(k, v) \
     if (a.prof && blockIdx.x == a.prof_cta && warp == 12 && lane == 0 && ub < 16) a.prof[608 + ub * 8 + (k)] = (v)
 #define UPROF(k) \
@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         for (int i = 0; i < L::EPI_STAGES; ++i) {
             tc::mbar_init(&epi_full[i], 1);
-            tc::mbar_init(&epi_empty[i], 1 + kEpiWarps);  // expand-MMA commit + every epilogue warp
+            tc::mbar_init(&epi_empty[i], 1 + kEpiWarps / 2);  // expand-MMA commit + the owning group's warps
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&s_full[b], 1);
@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::mbar_init(&v_full[b], 4);
             tc::mbar_init(&v_empty[b], 1);
             tc::mbar_init(&d_full[b], 1);
-            tc::mbar_init(&d_empty[b], kEpiWarps);
+            tc::mbar_init(&d_empty[b], kEpiWarps / 2);  // D buffer b belongs to epilogue group b
             tc::mbar_init(&p_full[b], 4);             // the 4 local V warps (expect_tx of the peers' st.async bytes)
             tc::mbar_init(&p_empty[b], 4 * (C - 1));  // the 4 V warps of each peer
         }
@@ -461,8 +461,12 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
     } else {
         // ------------------------------------------------ epilogue (warps 4..11)
-        const int q = warp & 3;          // the TMEM lane quadrant this warp may access
-        const int hf = (warp - 4) >> 2;  // which 64-column half of each 128-column chunk
+        // two groups of four warps take alternate chunks (group g: the chunks with
+        // dc % 2 == g, hence D buffer g and the stages of parity g); a warp covers
+        // its TMEM lane quadrant's 16 rows across the whole 128-column chunk, so two
+        // chunks' latency chains (TMEM load, smem RMW, TMA store) overlap
+        const int q = warp & 3;             // the TMEM lane quadrant this warp may access
+        const int grp = (warp - 4) >> 2;    // chunk parity this group owns
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         const uint64_t stream = (a.flags & 16) ? tc::policy_evict_normal() : tc::policy_evict_first();
         int stage = 0, ub = 0, dc = 0, pend = -1;
@@ -470,108 +474,121 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         for (int u = u0; u < u1; ++u) {
             const int4 U = a.units[u];
             if (U.x < a.slot_base) continue;
-            const int slot = U.x - a.slot_base, nch = U.z;
+            const int nch = U.z;
             const int2 ch = q < nch ? a.chunks[U.y + q] : make_int2(0, 0);
-            const int sb = ub & 1;
             const int r1 = lane >> 2, cp = 2 * (lane & 3);
-            for (int j = 0; j < NJ; ++j) {
-                const int db = dc & 1;
+            for (int j = 0; j < NJ; ++j, ++dc) {
+                const int st0 = stage;
+                const uint32_t ph0 = phase;
+                if (++stage == L::EPI_STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+                if ((dc & 1) != grp) continue;
+                const int db = grp;
                 tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
                 PROF(3);
-                tc::mbar_wait(&epi_full[stage], phase);
+                tc::mbar_wait(&epi_full[st0], ph0);
                 PROF(4);
                 tc::fence_after_sync();
-                uint32_t v[32];
-                tc::tmem_ld_16x256b_x8(tmem + lane_base + L::D_COL0 + db * kEpiN + hf * 64, v);
-                tc::tmem_ld_wait();
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&d_empty[db]);
-                PROF(5);
-                const uint32_t panel = L::OFF_EPI + stage * L::EPI_STAGE + hf * L::H_BYTES;
-                if (ch.y > 0 && (a.flags & 32)) {
-                    // reduce epilogue: stage the bf16 delta (-0.0 in rows past the
-                    // chunk: the additive identity that keeps every bit, -0.0
-                    // included) and let TMA add it into h in L2
+#pragma unroll 1
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t v[32];
+                    tc::tmem_ld_16x256b_x8(tmem + lane_base + L::D_COL0 + db * kEpiN + hf * 64, v);
+                    tc::tmem_ld_wait();
+                    if (hf == 1) {
+                        tc::fence_before_sync();
+                        __syncwarp();
+                        if (lane == 0) tc::mbar_arrive(&d_empty[db]);
+                        PROF(5);
+                    }
+                    const uint32_t panel = L::OFF_EPI + st0 * L::EPI_STAGE + hf * L::H_BYTES;
+                    if (ch.y > 0 && (a.flags & 32)) {
+                        // reduce epilogue: stage the bf16 delta (-0.0 in rows past the
+                        // chunk: the additive identity that keeps every bit, -0.0
+                        // included) and let TMA add it into h in L2
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int half = 0; half < 2; ++half) {
-                            const int rr = r1 + 8 * half;
-                            const uint32_t d = rr < ch.y ? f32x2_to_bf16(__uint_as_float(v[4 * i + 2 * half]),
-                                                                          __uint_as_float(v[4 * i + 2 * half + 1]))
-                                                         : 0x80008000u;
-                            *reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(q * kChunk + rr, 8 * i + cp, 64)) = d;
-                        }
-                    tc::fence_proxy_async();
-                    __syncwarp();
-                    if (lane == 0)
-                        tc::tma_reduce_add_2d(&tmH, (jc0 + j) * kEpiN + hf * 64, ch.x, sbase + panel + q * (kChunk * 128));
-                } else if (ch.y > 0) {
-                    // all 16 loads first, then the math, then the stores (the
-                    // addresses are disjoint but not provably so to the compiler)
-                    uint32_t hv[16];
+                            for (int half = 0; half < 2; ++half) {
+                                const int rr = r1 + 8 * half;
+                                const uint32_t d = rr < ch.y ? f32x2_to_bf16(__uint_as_float(v[4 * i + 2 * half]),
+                                                                              __uint_as_float(v[4 * i + 2 * half + 1]))
+                                                             : 0x80008000u;
+                                *reinterpret_cast<uint32_t*>(sgen + panel +
+                                                             tc::sw128_offset(q * kChunk + rr, 8 * i + cp, 64)) = d;
+                            }
+                    } else if (ch.y > 0) {
+                        // all 16 loads first, then the math, then the stores (the
+                        // addresses are disjoint but not provably so to the compiler)
+                        uint32_t hv[16];
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int half = 0; half < 2; ++half)
-                            hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
-                                sgen + panel + tc::sw128_offset(q * kChunk + r1 + 8 * half, 8 * i + cp, 64));
+                            for (int half = 0; half < 2; ++half)
+                                hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
+                                    sgen + panel + tc::sw128_offset(q * kChunk + r1 + 8 * half, 8 * i + cp, 64));
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int half = 0; half < 2; ++half) {
-                            float lo, hi;
-                            bf16x2_to_acc(hv[2 * i + half], lo, hi);
-                            lo += __uint_as_float(v[4 * i + 2 * half]);
-                            hi += __uint_as_float(v[4 * i + 2 * half + 1]);
-                            hv[2 * i + half] = f32x2_to_bf16(lo, hi);
-                        }
+                            for (int half = 0; half < 2; ++half) {
+                                float lo, hi;
+                                bf16x2_to_acc(hv[2 * i + half], lo, hi);
+                                lo += __uint_as_float(v[4 * i + 2 * half]);
+                                hi += __uint_as_float(v[4 * i + 2 * half + 1]);
+                                hv[2 * i + half] = f32x2_to_bf16(lo, hi);
+                            }
 #pragma unroll
-                    for (int i = 0; i < 8; ++i)
+                        for (int i = 0; i < 8; ++i)
 #pragma unroll
-                        for (int half = 0; half < 2; ++half)
-                            *reinterpret_cast<uint32_t*>(sgen + panel +
-                                                         tc::sw128_offset(q * kChunk + r1 + 8 * half, 8 * i + cp, 64)) =
-                                hv[2 * i + half];
-                    tc::fence_proxy_async();  // epilogue smem writes -> TMA store reads
+                            for (int half = 0; half < 2; ++half)
+                                *reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(q * kChunk + r1 + 8 * half,
+                                                                                             8 * i + cp, 64)) =
+                                    hv[2 * i + half];
+                    }
+                }
+                if (ch.y > 0) {
+                    tc::fence_proxy_async();  // epilogue smem writes -> TMA reads
                     __syncwarp();
                     PROF(6);
-                    if (ch.y == kChunk) {
+                    const uint32_t panel0 = L::OFF_EPI + st0 * L::EPI_STAGE;
+                    if (a.flags & 32) {
                         if (lane == 0)
-                            tc::tma_store_2d_hint(&tmH, (jc0 + j) * kEpiN + hf * 64, ch.x,
-                                                  sbase + panel + q * (kChunk * 128), stream);
+                            for (int hf = 0; hf < 2; ++hf)
+                                tc::tma_reduce_add_2d(&tmH, (jc0 + j) * kEpiN + hf * 64, ch.x,
+                                                      sbase + panel0 + hf * L::H_BYTES + q * (kChunk * 128));
+                    } else if (ch.y == kChunk) {
+                        if (lane == 0)
+                            for (int hf = 0; hf < 2; ++hf)
+                                tc::tma_store_2d_hint(&tmH, (jc0 + j) * kEpiN + hf * 64, ch.x,
+                                                      sbase + panel0 + hf * L::H_BYTES + q * (kChunk * 128), stream);
                     } else {
                         // partial chunk (end of a prompt): only its valid rows go back
-                        for (int idx = lane; idx < ch.y * 8; idx += 32) {
-                            const int rr = idx >> 3, c16 = idx & 7;
+                        for (int idx = lane; idx < ch.y * 16; idx += 32) {
+                            const int rr = idx >> 4, hf = (idx >> 3) & 1, c16 = idx & 7;
                             const uint4 val = *reinterpret_cast<const uint4*>(
-                                sgen + panel + tc::sw128_offset(q * kChunk + rr, c16 * 8, 64));
+                                sgen + panel0 + hf * L::H_BYTES + tc::sw128_offset(q * kChunk + rr, c16 * 8, 64));
                             *reinterpret_cast<uint4*>(a.h + static_cast<long long>(ch.x + rr) * a.ldh +
                                                       (jc0 + j) * kEpiN + hf * 64 + c16 * 8) = val;
                         }
                     }
                 }
                 if (lane == 0) {
-                    // release the PREVIOUS stage once its store has read shared memory
                     tc::tma_store_commit();
                     if (a.flags & 1) {
+                        // release this stage once its stores have read shared memory
                         tc::tma_store_wait_read();
-                        tc::mbar_arrive(&epi_empty[stage]);
+                        tc::mbar_arrive(&epi_empty[st0]);
                     } else {
+                        // release the group's PREVIOUS stage once its stores have read
                         tc::tma_store_wait_read_1();
                         if (pend >= 0) tc::mbar_arrive(&epi_empty[pend]);
-                        pend = stage;
+                        pend = st0;
                     }
-                    if (warp == 4) atomicAdd(&s_epi_done, 1);
+                    if (q == 0) atomicAdd(&s_epi_done, 1);
                 }
                 __syncwarp();
                 PROF(7);
-                if (++stage == L::EPI_STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-                ++dc;
             }
             ++ub;
         }
@@ -597,7 +614,9 @@ void reft_tc_set_flags(int flags, int look) {
 }
 static long long* g_tc_prof = nullptr;
 int reft_tc_last_grid() { return g_tc_last_grid; }
+void reft_tc_note_grid(int grid) { g_tc_last_grid = grid; }
 void reft_tc_set_profile(long long* buf) { g_tc_prof = buf; }
+long long* reft_tc_profile_buffer() { return g_tc_prof; }
 
 template <int R, int C>
 static int launch_reft_tc(const ReftTcArgs& args, const CUtensorMap& tmH, const CUtensorMap& tmA, int num_sms,

@@ -66,14 +66,16 @@ def test_zero_delta_adapters_leave_stream_bit_identical(cuda_device, kind):
     assert torch.equal(h, h0)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2, 3])
 @pytest.mark.parametrize("rank", [16, 32])
 @pytest.mark.parametrize("d", [128, 1024, 2048, 4096, 8192])
 def test_tensor_core_and_simt_variants(cuda_device, variant, rank, d):
-    """The tcgen05 kernel (variant 1) and the SIMT kernel (variant 0) on the
-    same mixed batch: short (partial-chunk) and multi-unit segments, decode
-    and adapter-less entries, and LoRA-class tokens interleaved in the sorted
-    list (the ReFT kernel must skip their units)."""
+    """The tcgen05 kernels (1 automatic, 2 streaming, 3 resident) and the SIMT
+    kernel (0) on the same mixed batch: short (partial-chunk) and multi-unit
+    segments, decode and adapter-less entries, and LoRA-class tokens
+    interleaved in the sorted list (the ReFT kernel must skip their units)."""
+    if variant == 3 and not (d % 1024 == 0 and d // 1024 in ((1, 2, 4, 8) if rank == 16 else (1, 2, 4))):
+        pytest.skip("the resident kernel covers d = 1024 * {1, 2, 4, 8} (r = 32: up to 4096)")
     from paper_2605_14217_b200 import _lib
     from paper_2605_14217_b200.meta import BatchMeta
     from paper_2605_14217_b200.ops import apply_lora_, apply_reft_

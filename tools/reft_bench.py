@@ -22,7 +22,7 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 
 
-def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False):
+def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False, d=4096):
     import torch
 
     from paper_2605_14217_b200 import AdapterKind, _lib
@@ -31,7 +31,6 @@ def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False):
     from paper_2605_14217_b200.pool import AdapterPool
 
     dev = torch.device("cuda", 0)
-    d = 4096
     n_ad = int(max(ids)) + 1
     pool = AdapterPool(1, d, reft_capacity=n_ad, reft_rank=rank, dtype=torch.bfloat16, device=dev)
     pool.fill_synthetic_(n_ad, AdapterKind(kind), rank, seed=1)
@@ -58,6 +57,37 @@ def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False):
     finally:
         lib.preft_set_reft_variant(-1)
     us = float(np.mean([a.elapsed_time(b) for a, b in ev]) * 1e3)
+    grid = int(lib.preft_diag_reft_tc(None))
+    if prof and variant == 3:
+        import ctypes
+
+        buf = torch.zeros(736, dtype=torch.int64, device=dev)
+        lib.preft_set_reft_variant(3)
+        lib.preft_diag_reft_tc(ctypes.c_void_p(buf.data_ptr()))
+        apply_reft_(hs[0], meta, pool, 0)
+        torch.cuda.synchronize()
+        lib.preft_diag_reft_tc(None)
+        lib.preft_set_reft_variant(-1)
+        st = buf.cpu().numpy().astype(np.int64)
+        un = st[:128].reshape(16, 8)
+        ch = st[128:640].reshape(64, 8)
+        t0 = int(un[0, 5])
+        sx = st[640:704].reshape(16, 4)
+        print("units: s_full p_full v_full | mma first last | prod first last | stash first(h_full, t_empty) last(h_full, t_empty)", file=sys.stderr)
+        for u in range(16):
+            if un[u, 5]:
+                r = [int(un[u, k]) - t0 if un[u, k] else -1 for k in (0, 1, 2, 3, 4, 5, 6)]
+                x = [int(v) - t0 if v else -1 for v in sx[u]]
+                print(u, r[:3], "|", r[3:5], "|", r[5:7], "|", x, file=sys.stderr)
+        print("stash panels: waits done, released", file=sys.stderr)
+        for c in range(48):
+            if ch[c, 6]:
+                print("  p", c, int(ch[c, 6]) - t0, int(ch[c, 7]) - t0, file=sys.stderr)
+        print("chunks: epi d_full rmw released | mma bt_full d_empty issued", file=sys.stderr)
+        for c in range(48):
+            if ch[c, 3]:
+                r = [int(ch[c, k]) - t0 if ch[c, k] else -1 for k in (0, 1, 2, 3, 4, 5)]
+                print(c, r[:3], "|", r[3:], file=sys.stderr)
     if prof and variant == 1:
         import ctypes
 
@@ -88,8 +118,8 @@ def run(kind, rank, lens, ids, variant, peak, iters=10, prof=False):
     distinct = len(set(int(i) for i in ids))
     alg = T * 2 * d * 2 + distinct * 2 * (2 * rank * d) + distinct * 4 * rank
     gbs = alg / us / 1e3
-    return {"kind": kind, "rank": rank, "tokens": T, "distinct": distinct, "variant": "tc" if variant == 1 else "simt",
-            "us": round(us, 1), "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
+    return {"kind": kind, "rank": rank, "d": d, "tokens": T, "distinct": distinct, "variant": ["simt", "tc", "pass", "res"][variant],
+            "us": round(us, 1), "grid": grid, "gbs": round(gbs, 1), "frac": round(gbs / peak, 4),
             "tokens_per_s_32_layers": round(T / (us * 1e-6) / 32, 1)}
 
 
@@ -97,10 +127,26 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--peak", type=float, default=None)
     p.add_argument("--case", choices=["cfg3", "cfg5", "all"], default="all")
-    p.add_argument("--variant", choices=["tc", "simt", "all"], default="all")
+    p.add_argument("--variant", choices=["tc", "simt", "pass", "res", "all"], default="all")
     p.add_argument("--iters", type=int, default=10)
     p.add_argument("--prof", action="store_true")
+    p.add_argument("--d", type=int, default=4096, help="hidden size (8B shape: 4096)")
+    p.add_argument("--persist-mb", type=float, default=None, help="L2 set-aside for persisting (evict_last) lines")
     args = p.parse_args()
+    if args.persist_mb is not None:
+        import ctypes
+
+        import torch
+
+        torch.cuda.init()
+        rt = ctypes.CDLL("libcudart.so.12")
+        mx = ctypes.c_int()
+        rt.cudaDeviceGetAttribute(ctypes.byref(mx), 108, 0)  # cudaDevAttrMaxPersistingL2CacheSize
+        want = min(int(args.persist_mb * 2**20), mx.value)
+        rc = rt.cudaDeviceSetLimit(6, ctypes.c_size_t(want))  # cudaLimitPersistingL2CacheSize
+        got = ctypes.c_size_t()
+        rt.cudaDeviceGetLimit(ctypes.byref(got), 6)
+        print(f"persisting L2: max {mx.value >> 20} MB, set rc={rc}, now {got.value >> 20} MB", file=sys.stderr)
     peak = args.peak
     if peak is None:
         f = ROOT / "MEASURED_PEAKS.json"
@@ -109,11 +155,11 @@ def main():
     cfg3 = ([2048] * 32, rng.integers(0, 512, size=32))
     w = 1.0 / (np.arange(512) + 1.0)
     cfg5 = (list(rng.integers(8192, 16385, size=8)), rng.choice(512, size=8, p=w / w.sum()))
-    for variant in {"tc": (1,), "simt": (0,), "all": (1, 0)}[args.variant]:
+    for variant in {"tc": (1,), "simt": (0,), "pass": (2,), "res": (3,), "all": (1, 0)}[args.variant]:
         if args.case in ("cfg3", "all"):
-            print(json.dumps(run("direft", 16, *cfg3, variant, peak, args.iters, args.prof)), flush=True)
+            print(json.dumps(run("direft", 16, *cfg3, variant, peak, args.iters, args.prof, args.d)), flush=True)
         if args.case in ("cfg5", "all"):
-            print(json.dumps(run("loreft", 32, *cfg5, variant, peak, args.iters, args.prof)), flush=True)
+            print(json.dumps(run("loreft", 32, *cfg5, variant, peak, args.iters, args.prof, args.d)), flush=True)
 
 
 if __name__ == "__main__":
