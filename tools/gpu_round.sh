@@ -30,6 +30,9 @@ PY
 timeout 300 python tools/kbench.py > $O/${TAG}_kbench.json 2> $O/${TAG}_kbench.err
 timeout 300 python tools/kbench.py --requests 32 --decodes 32 > $O/${TAG}_kbench_small.json 2>> $O/${TAG}_kbench.err
 timeout 300 python tools/reft_bench.py > $O/${TAG}_reft.json 2>> $O/${TAG}_kbench.err
+for d in 2048 4096; do for v in pass res; do
+  timeout 200 python tools/reft_bench.py --variant $v --d $d --iters 20 >> $O/${TAG}_reft_variants.json 2>> $O/${TAG}_kbench.err
+done; done
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"lora|meta|reft" -c 390 --csv \
   --log-file $O/${TAG}_launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-punica-step --no-secondary \
   > /dev/null 2>&1
@@ -42,7 +45,9 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:reft
 timeout 400 ncu --set full --clock-control none -k regex:"shrink_tc|expand_tc" -s 8 -c 8 -o $O/${TAG}_split_prof \
   python tools/tp_bench.py > /dev/null 2>&1
 # full reports are large (the 64 MiB return limit): keep CSV exports of the secondary captures
-for r in reft_prof split_prof; do
+timeout 300 ncu --set full --clock-control none --import-source on -k regex:reft_res -s 3 -c 1 -o $O/${TAG}_res_prof \
+  python tools/reft_bench.py --case cfg3 --variant res --d 2048 --iters 1 > /dev/null 2>&1
+for r in reft_prof split_prof res_prof; do
   ncu -i $O/${TAG}_${r}.ncu-rep --page raw --csv > $O/${TAG}_${r}_raw.csv 2>/dev/null
   python tools/ncu_metrics.py $O/${TAG}_${r}.ncu-rep > $O/${TAG}_${r}_metrics.txt 2>/dev/null
   rm -f $O/${TAG}_${r}.ncu-rep
