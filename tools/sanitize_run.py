@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """Small invocations of every kernel family for compute-sanitizer runs:
-K1, K2 (team, warp, f64), K2 split (tcgen05 + SIMT), K3 (SIMT + tcgen05), K4."""
+K1, K2 (team, warp, f64), K2 split (tcgen05 + SIMT), K3 (SIMT + tcgen05 streaming +
+tcgen05 TMEM-parked at d = 1024 / 2048), K4."""
 import sys
 from pathlib import Path
 
@@ -46,6 +47,25 @@ def main():
         apply_reft_(h, meta, pool, 0)
         torch.cuda.synchronize()
         print("ok", dtype, lr, rr)
+    lib = _lib.load()
+    for d, rr in ((1024, 16), (2048, 32)):
+        pool = AdapterPool(1, d, reft_capacity=3, reft_rank=rr, dtype=torch.bfloat16, device=dev)
+        for a in range(3):
+            pool.register(U.random_reft_adapter(rng, a, 1, d, rr, AdapterKind.LOREFT))
+        lens = [1] * 4 + list(rng.integers(1, 70, size=6)) + [130]
+        qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+        ids = [[0, 1, 2, None][int(i) % 4] for i in range(len(lens))]
+        flags = np.array([_lib.ENTRY_DECODE] * 4 + [0] * (len(lens) - 4), np.int32)
+        meta = BatchMeta(16, int(qsl[-1]), device=dev)
+        U.stage(meta, pool, qsl, ids, flags)
+        h = U.rand_act(rng, int(qsl[-1]), d, torch.bfloat16, dev)
+        assert lib.preft_set_reft_variant(3) == 0
+        try:
+            apply_reft_(h, meta, pool, 0)
+            torch.cuda.synchronize()
+        finally:
+            lib.preft_set_reft_variant(-1)
+        print("ok resident", d, rr)
 
 
 if __name__ == "__main__":
