@@ -182,10 +182,74 @@ static bool aligned16r(const void* p) { return (reinterpret_cast<uintptr_t>(p) &
 int grid_for(const void* fn, int threads, int num_sms);
 
 int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A, const void* Bt,
-                  const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms);
+                  const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms, int part_lo,
+                  int part_hi);
 int reft_res_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A,
-                   const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms);
+                   const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms,
+                   int part_lo, int part_hi, bool dry);
 bool reft_res_preferred(int d, int r);
+bool reft_res_eligible(int d, int r);
+
+// Co-launch (d = 4096): clusters of d/1024 CTAs for the TMEM-parked kernel
+// pack only ~132 of the 148 SMs, so the streaming kernel runs on the SMs left
+// over, on a forked stream, over the last part of the unit list (the units
+// split in proportion to the two kernels' per-SM rates).  Env
+// PREFT_REFT_COLAUNCH=0 disables, PREFT_REFT_COSPLIT=<fraction*4096 for the
+// parked kernel> overrides the split.
+struct CoStreams {
+    int device = -1;
+    cudaStream_t aux = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+static CoStreams g_co[16];
+
+static CoStreams* co_streams() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    CoStreams& c = g_co[dev];
+    if (c.device < 0) {
+        if (cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        c.device = dev;
+    }
+    return &c;
+}
+
+static int colaunch_split() {
+    static int v = -2;
+    if (v == -2) {
+        const char* off = getenv("PREFT_REFT_COLAUNCH");
+        const char* sp = getenv("PREFT_REFT_COSPLIT");
+        v = (off && off[0] == '0') ? -1 : sp ? atoi(sp) : 0;
+    }
+    return v;  // -1 off, 0 automatic, else the parked kernel's share in 1/4096
+}
+
+static int reft_colaunch(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A,
+                         const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream,
+                         int num_sms) {
+    const int sp = colaunch_split();
+    // measured win at clusters of 4 (d = 4096, r = 16: 68% vs 65%); clusters of 8 run the
+    // parked kernel at 54% and would drag the pair down
+    if (sp < 0 || !reft_res_eligible(d, r) || d / 1024 != 4) return PREFT_ERR_SHAPE;
+    const int g = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms, 0, 4096, true);
+    const int left = num_sms - g;  // (a dry run returns the grid; error codes are < 32)
+    if (g < 32 || left < 2) return PREFT_ERR_SHAPE;
+    CoStreams* c = co_streams();
+    if (!c) return PREFT_ERR_SHAPE;
+    // per-SM rate of the parked kernel ~1.2x the streaming kernel's (no L2 re-read misses)
+    const int f = sp > 0 ? min(4095, sp) : static_cast<int>(4096.0 * 1.2 * g / (1.2 * g + left));
+    if (cudaEventRecord(c->fork, stream) != cudaSuccess) return PREFT_ERR_CONFIG;
+    if (cudaStreamWaitEvent(c->aux, c->fork, 0) != cudaSuccess) return PREFT_ERR_CONFIG;
+    int rc = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms, 0, f, false);
+    const int rc2 = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, c->aux, left, f, 4096);
+    // always join, so a failed half never leaves the aux stream forked off a capture
+    cudaEventRecord(c->join, c->aux);
+    cudaStreamWaitEvent(stream, c->join, 0);
+    if (rc == PREFT_OK) rc = rc2;
+    return rc;
+}
 
 // -1 automatic (tensor cores when eligible), 0 SIMT only, 1 tensor cores only
 // (resident kernel when eligible, else streaming), 2 streaming tensor-core
@@ -210,9 +274,13 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
     if (variant != 0 && Bt && dtype == PREFT_DTYPE_BF16) {
         int rc = PREFT_ERR_SHAPE;
         if (variant == 3 || (variant != 2 && reft_res_preferred(d, r)))
-            rc = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms);
+            rc = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms, 0, 4096, false);
         if (rc != PREFT_ERR_SHAPE || variant == 3) return rc;  // launched, failed, or resident forced
-        rc = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms);
+        if (variant != 2 && r == 16) {
+            rc = reft_colaunch(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms);
+            if (rc != PREFT_ERR_SHAPE) return rc;
+        }
+        rc = reft_tc_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms, 0, 4096);
         if (rc != PREFT_ERR_SHAPE || variant >= 1) return rc;  // launched, failed, or TC forced
     } else if (variant >= 1) {
         return PREFT_ERR_SHAPE;

@@ -100,6 +100,7 @@ struct ResArgs {
     unsigned char* xs;
     long long* prof;  // diagnostics: clock64 stamps of CTA prof_cta (NULL in production)
     int prof_cta;
+    int part_lo, part_hi;  // this launch takes units [N*lo/4096, N*hi/4096) (co-launch split)
 };
 
 constexpr int kXsHeader = 256;
@@ -191,7 +192,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     unsigned long long epoch = 0;
     if constexpr (XG && C > 1) epoch = *reinterpret_cast<volatile unsigned long long*>(a.xs) << 32;
     int u0, u1;
-    even_share(a.counters[PREFT_CTR_UNITS], blockIdx.x / C, gridDim.x / C, u0, u1);  // contiguous runs share adapters
+    {
+        const long long nu = a.counters[PREFT_CTR_UNITS];
+        const int ulo = static_cast<int>(nu * a.part_lo >> 12), uhi = static_cast<int>(nu * a.part_hi >> 12);
+        even_share(uhi - ulo, blockIdx.x / C, gridDim.x / C, u0, u1);  // contiguous runs share adapters
+        u0 += ulo;
+        u1 += ulo;
+    }
     const int pc0 = crank * NP, jc0 = crank * NJ;  // first global panel / chunk of this CTA
     const int r1 = lane >> 2, cp = 2 * (lane & 3);   // 16x256b layout: rows r1, r1 + 8; columns 8i + cp + {0, 1}
 
@@ -645,7 +652,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int R, int C, int COLS, bool XG>
 int launch_res(const ResArgs& args, const CUtensorMap& tmH, const CUtensorMap& tmH64, const CUtensorMap& tmA, int num_sms,
-               cudaStream_t stream) {
+               cudaStream_t stream, bool dry = false) {
     auto fn = reft_res_kernel<R, C, COLS, XG>;
     const int smem = ResLayout<R, C, COLS, XG>::SMEM;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -678,6 +685,7 @@ int launch_res(const ResArgs& args, const CUtensorMap& tmH, const CUtensorMap& t
         }
         grid = min(grid, nc * C);
     }
+    if (dry) return grid;
     cfg.gridDim = dim3(grid);
     reft_tc_note_grid(grid);
     e = cudaLaunchKernelEx(&cfg, fn, tmH, tmH64, tmA, args);
@@ -757,7 +765,8 @@ static int xs_for(cudaStream_t stream, int num_sms, unsigned char** out) {
 }
 
 int reft_res_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A,
-                   const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms) {
+                   const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms,
+                   int part_lo, int part_hi, bool dry) {
     if (!Bt || !reft_res_eligible(d, r) || rows < 1) return PREFT_ERR_SHAPE;
     if (!meta->chunks || !meta->units || (ldh % 8) || (reinterpret_cast<uintptr_t>(h) & 15) ||
         (reinterpret_cast<uintptr_t>(A) & 15) || (reinterpret_cast<uintptr_t>(Bt) & 15))
@@ -782,6 +791,8 @@ int reft_res_apply(const preft_meta_t* meta, void* h, long long rows, long long 
     args.chunks = reinterpret_cast<const int2*>(meta->chunks);
     args.units = reinterpret_cast<const int4*>(meta->units);
     args.counters = meta->counters;
+    args.part_lo = part_lo;
+    args.part_hi = part_hi;
     args.prof = reft_tc_profile_buffer();
     {
         const char* pc = args.prof ? getenv("PREFT_REFT_PROF_CTA") : nullptr;
@@ -790,12 +801,12 @@ int reft_res_apply(const preft_meta_t* meta, void* h, long long rows, long long 
     const int c = d / kCols;
     const bool xg = c > 1 && res_xchg_l2();
     args.xs = nullptr;
-    if (xg) {
+    if (xg && !dry) {
         const int rc = xs_for(stream, num_sms, &args.xs);
         if (rc != PREFT_OK) return rc;
     }
 #define PREFT_RES(RR, CC, XG_) \
-    if (r == RR && c == CC && xg == XG_) return launch_res<RR, CC, kCols, XG_>(args, tmH, tmH64, tmA, num_sms, stream);
+    if (r == RR && c == CC && xg == XG_) return launch_res<RR, CC, kCols, XG_>(args, tmH, tmH64, tmA, num_sms, stream, dry);
     PREFT_RES(16, 1, false)
     PREFT_RES(16, 2, false)
     PREFT_RES(16, 4, false)

@@ -104,6 +104,7 @@ struct ReftTcArgs {
     int look;   // with bit 1: panels the shrink may run ahead of the epilogue's re-read
     long long* prof;  // diagnostics: clock64 stamps of CTA prof_cta (NULL in production)
     int prof_cta;
+    int part_lo, part_hi;  // this launch takes units [N*lo/4096, N*hi/4096) (co-launch split)
 };
 
 // diagnostics: warp 4 lane 0 of CTA 0 stamps chunk phases (first 64 chunks) and unit phases
@@ -168,7 +169,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // a cluster of C CTAs owns each unit; CTA `crank` owns columns [crank*d/C, (crank+1)*d/C)
     const int crank = C > 1 ? static_cast<int>(tc::cluster_ctarank()) : 0;
     int u0, u1;
-    even_share(a.counters[PREFT_CTR_UNITS], blockIdx.x / C, gridDim.x / C, u0, u1);  // contiguous runs share adapters
+    {
+        const long long nu = a.counters[PREFT_CTR_UNITS];
+        const int ulo = static_cast<int>(nu * a.part_lo >> 12), uhi = static_cast<int>(nu * a.part_hi >> 12);
+        even_share(uhi - ulo, blockIdx.x / C, gridDim.x / C, u0, u1);  // contiguous runs share adapters
+        u0 += ulo;
+        u1 += ulo;
+    }
     const int NP = a.d / (64 * C), NJ = a.d / (kEpiN * C);
     const int pc0 = crank * NP, jc0 = crank * NJ;  // first global panel / chunk of this CTA
 
@@ -671,7 +678,8 @@ static int tc_cluster_for(int d) {
 
 // returns 0 on launch, PREFT_ERR_SHAPE if the shape is not TC-eligible, or -cudaError
 int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh, int d, const void* A,
-                  const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms) {
+                  const void* Bt, const void* bias, const void* scale, int r, cudaStream_t stream, int num_sms,
+                  int part_lo, int part_hi) {
     if (!Bt || (r != 16 && r != 32) || d < 128 || d % 128 || rows < 1) return PREFT_ERR_SHAPE;
     if ((d / tc_cluster_for(d)) % (64 * spps_for(r, tc_cluster_for(d)))) return PREFT_ERR_SHAPE;
     if (!meta->chunks || !meta->units || (ldh % 8) || (reinterpret_cast<uintptr_t>(h) & 15) ||
@@ -697,6 +705,8 @@ int reft_tc_apply(const preft_meta_t* meta, void* h, long long rows, long long l
     args.chunks = reinterpret_cast<const int2*>(meta->chunks);
     args.units = reinterpret_cast<const int4*>(meta->units);
     args.counters = meta->counters;
+    args.part_lo = part_lo;
+    args.part_hi = part_hi;
     {
         int& flags = g_tc_flags;
         int& look = g_tc_look;
