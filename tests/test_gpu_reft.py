@@ -199,3 +199,54 @@ def test_tensor_core_pipeline_knobs_keep_results(cuda_device, flags):
     assert torch.equal(h[3, 5].view(torch.int16), neg0.view(torch.int16))
     ref = U.reft_oracle(h_in, qsl, slots, flags_e, pool, 0)
     helpers.check_close(out, h_in, ref, "bf16", f"reft knobs {flags}")
+
+
+def test_colaunch_eager_and_graph(cuda_device):
+    """d = 4096, r = 16 runs the TMEM-parked kernel and the streaming kernel at
+    once (forked stream, unit list split).  The result matches the oracle (and
+    the streaming kernel alone within the same tolerance: the two sum the
+    shrink partials in different orders), and a CUDA graph that captured the
+    fork/join replays it bit for bit."""
+    from paper_2605_14217_b200 import _lib
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_reft_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(7)
+    d = 4096
+    pool = AdapterPool(1, d, reft_capacity=6, reft_rank=16, dtype=torch.bfloat16, device=cuda_device)
+    for aid in range(6):
+        pool.register(U.random_reft_adapter(rng, aid, 1, d, 16, AdapterKind.DIREFT if aid % 2 else AdapterKind.LOREFT))
+    lens = [1] * 8 + list(rng.integers(1, 300, size=24)) + [2048, 1024]
+    qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    ids = [int(i) % 6 if i % 5 else None for i in range(len(lens))]
+    flags = np.array([_lib.ENTRY_DECODE] * 8 + [0] * (len(lens) - 8), dtype=np.int32)
+    meta = BatchMeta(64, int(qsl[-1]), device=cuda_device)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    h0 = U.rand_act(rng, int(qsl[-1]), d, torch.bfloat16, cuda_device)
+    h_in = U.to_np(h0)
+    mask = U.oracle_mask(qsl, slots, flags)
+    ref = U.reft_oracle(h_in, qsl, slots, flags, pool, 0)
+    lib = _lib.load()
+    try:
+        assert lib.preft_set_reft_variant(-1) == 0
+        h_co = h0.clone()
+        apply_reft_(h_co, meta, pool, 0)
+        torch.cuda.synchronize()
+        out = U.to_np(h_co)
+        assert np.array_equal(out[~mask], h_in[~mask])
+        helpers.check_close(out, h_in, ref, "bf16", "reft co-launch d=4096 r=16")
+        h_g = h0.clone()
+        s = torch.cuda.Stream(cuda_device)
+        s.wait_stream(torch.cuda.current_stream(cuda_device))
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            apply_reft_(h_g, meta, pool, 0)
+        for _ in range(2):
+            h_g.copy_(h0)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            assert torch.equal(h_g.view(torch.int16), h_co.view(torch.int16))
+    finally:
+        lib.preft_set_reft_variant(-1)
