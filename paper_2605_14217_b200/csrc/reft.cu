@@ -12,6 +12,8 @@
 // used for the shrink and updated in registers for the expand, so h moves
 // HBM->SM->HBM exactly once — the algorithmic minimum 2*d*e bytes per token.
 // Wider rows re-read h for the expand (an L1/L2 hit in practice).
+#include <mutex>
+
 #include "common.cuh"
 
 namespace preft {
@@ -203,9 +205,12 @@ struct CoStreams {
 };
 static CoStreams g_co[16];
 
+static std::mutex g_co_mu;
+
 static CoStreams* co_streams() {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    std::lock_guard<std::mutex> lk(g_co_mu);
     CoStreams& c = g_co[dev];
     if (c.device < 0) {
         if (cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
