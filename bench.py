@@ -838,7 +838,7 @@ def run_ours(args):
             },
             "roofline": {
                 "bound": "hbm",
-                "kernel": "lora_kernel<bf16,VEC,R=1,NS=2> (gate/up fused group)",
+                "kernel": "lora_team_kernel<bf16,R=1,NS=2,U=4,TEAM=1> (K2, gate/up fused group)",
                 "achieved": round(achieved, 1),
                 "peak": peak,
                 "peak_source": peak_src,
