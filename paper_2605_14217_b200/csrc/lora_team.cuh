@@ -82,13 +82,15 @@ __global__ void __launch_bounds__(kTeamCtaThreads, MINB) lora_team_kernel(const 
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        if (c0 + TT * u < mv) {
-                            acc_t xf[W], af[W];
-                            V::to_acc(xv[u], xf);
-                            V::to_acc(av[u], af);
+                        // branch-free: a clamped (duplicate) vector past the row end
+                        // contributes x = 0.  A branch here let the compiler sink each
+                        // u's x load into its branch, serialising the batch's round trips
+                        const bool ok = c0 + TT * u < mv;
+                        acc_t xf[W], af[W];
+                        V::to_acc(xv[u], xf);
+                        V::to_acc(av[u], af);
 #pragma unroll
-                            for (int j = 0; j < W; ++j) acc[s][k] = macc(xf[j], af[j], acc[s][k]);
-                        }
+                        for (int j = 0; j < W; ++j) acc[s][k] = macc(ok ? xf[j] : acc_t(0), af[j], acc[s][k]);
                     }
                 }
             }
@@ -150,15 +152,21 @@ __global__ void __launch_bounds__(kTeamCtaThreads, MINB) lora_team_kernel(const 
                         const int c = min(c0 + TT * u, nv - 1);
                         bv[u] = V::ld_weight(Bs + static_cast<long long>(c) * W);
                     }
+                    // every u's update before any (predicated) store, so no load is
+                    // sunk behind a store branch
+                    acc_t yf[U][W];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        acc_t bf[W];
+                        V::to_acc(yv[u], yf[u]);
+                        V::to_acc(bv[u], bf);
+#pragma unroll
+                        for (int j = 0; j < W; ++j) yf[u][j] = macc(v[s], bf[j], yf[u][j]);
+                    }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
                         const int c = c0 + TT * u;
-                        acc_t yf[W], bf[W];
-                        V::to_acc(yv[u], yf);
-                        V::to_acc(bv[u], bf);
-#pragma unroll
-                        for (int j = 0; j < W; ++j) yf[j] = macc(v[s], bf[j], yf[j]);
-                        if (c < nv) V::st(yr + static_cast<long long>(c) * W, yf);
+                        if (c < nv) V::st(yr + static_cast<long long>(c) * W, yf[u]);
                     }
                 } else {
                     acc_t d[U][W];
@@ -184,14 +192,15 @@ __global__ void __launch_bounds__(kTeamCtaThreads, MINB) lora_team_kernel(const 
                     }
 #pragma unroll
                     for (int u = 0; u < U; ++u) {
-                        const int c = c0 + TT * u;
-                        if (c < nv) {
-                            acc_t yf[W];
-                            V::to_acc(yv[u], yf);
+                        acc_t yf[W];
+                        V::to_acc(yv[u], yf);  // outside the store branch: keeps the y load in the batch
 #pragma unroll
-                            for (int j = 0; j < W; ++j) yf[j] += d[u][j];
-                            V::st(yr + static_cast<long long>(c) * W, yf);
-                        }
+                        for (int j = 0; j < W; ++j) d[u][j] += yf[j];
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int c = c0 + TT * u;
+                        if (c < nv) V::st(yr + static_cast<long long>(c) * W, d[u]);
                     }
                 }
             }
