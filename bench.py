@@ -683,6 +683,14 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
     s = torch.cuda.current_stream(device)
     from paper_2605_14217_b200 import _lib
 
+    # the 128 site launches of a step as one CUDA graph (a serving engine's
+    # decode-graph practice); metadata is rebuilt eagerly before each replay
+    graph = None
+    try:
+        graph = plan.capture(run_meta=False)
+    except Exception:  # capture unsupported here: eager launches through the native plan
+        graph = None
+
     def run(limit=None):
         steps = toks = pre = 0
         for step in Scheduler(wl, cfg, PositionSchedule.PREFILL_ONLY):
@@ -693,7 +701,10 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
             if any(a is not None and not d for a, d in zip(step.adapter_ids, step.decode_flags)):
                 flags = (step.decode_flags * _lib.ENTRY_DECODE).astype(np.int32)
                 meta.build_arrays(step.qsl, pool.entry_arrays(step.qsl, step.adapter_ids, flags), flags, stream=s)
-                plan.run(s, run_meta=False)
+                if graph is not None:
+                    graph.replay()
+                else:
+                    plan.run(s, run_meta=False)
             steps += 1
             toks += step.tokens
             pre += step.prefill_tokens
@@ -714,8 +725,9 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
                        f"adapters, 8B shapes x 32 layers, max_batch 32, 32 device slots (LRU paging), budget 2048",
            "steps": steps, "tokens": toks, "prefill_tokens": pre, "ms": round(ms, 2),
            "value": round(toks / (ms / 1e3), 1), "unit": "tokens/s (prompt + generated)",
-           "page_ins": paged.page_ins - p0, "paged_gb": round((paged.paged_bytes - b0) / 1e9, 2)}
-    del plan, pool, paged, snaps
+           "page_ins": paged.page_ins - p0, "paged_gb": round((paged.paged_bytes - b0) / 1e9, 2),
+           "launch": "cuda graph per step (site launches), eager paging + K1" if graph is not None else "eager"}
+    del graph, plan, pool, paged, snaps
     torch.cuda.empty_cache()
     return out
 

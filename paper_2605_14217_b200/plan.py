@@ -105,15 +105,18 @@ class StepPlan:
         s = stream if stream is not None else torch.cuda.current_stream(self.pool.device)
         _lib.check(self.lib.preft_plan_run(self.handle, int(run_meta), ctypes.c_void_p(s.cuda_stream)), "plan_run")
 
-    def capture(self, stream=None) -> torch.cuda.CUDAGraph:
-        """Capture one run() into a CUDA graph (timing must be off)."""
+    def capture(self, stream=None, run_meta: bool = True) -> torch.cuda.CUDAGraph:
+        """Capture one run() into a CUDA graph (timing must be off).  With
+        run_meta=False the graph holds only the site launches: the caller
+        rebuilds the metadata (BatchMeta.build_arrays: H2D + K1) before each
+        replay, and the kernels read the new token counts from device memory."""
         s = stream if stream is not None else torch.cuda.Stream(self.pool.device)
         s.wait_stream(torch.cuda.current_stream(self.pool.device))
         with torch.cuda.stream(s):
-            self.run(s)  # warm-up: occupancy queries, smem attributes
+            self.run(s, run_meta)  # warm-up: occupancy queries, smem attributes
         torch.cuda.current_stream(self.pool.device).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            self.run(s)
+            self.run(s, run_meta)
         self.graph = g
         return g
