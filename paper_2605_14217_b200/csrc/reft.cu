@@ -207,12 +207,16 @@ static CoStreams g_co[16];
 
 static std::mutex g_co_mu;
 
-static CoStreams* co_streams() {
+static CoStreams* co_streams(cudaStream_t stream) {
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
     std::lock_guard<std::mutex> lk(g_co_mu);
     CoStreams& c = g_co[dev];
     if (c.device < 0) {
+        // creating streams/events is not allowed while a capture is open: the
+        // first co-launch must run eagerly (a warm-up); until then, one kernel
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
         if (cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
         if (cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
         if (cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
@@ -241,7 +245,7 @@ static int reft_colaunch(const preft_meta_t* meta, void* h, long long rows, long
     const int g = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms, 0, 4096, true);
     const int left = num_sms - g;  // (a dry run returns the grid; error codes are < 32)
     if (g < 32 || left < 2) return PREFT_ERR_SHAPE;
-    CoStreams* c = co_streams();
+    CoStreams* c = co_streams(stream);
     if (!c) return PREFT_ERR_SHAPE;
     // per-SM rate of the parked kernel ~1.2x the streaming kernel's (no L2 re-read misses)
     const int f = sp > 0 ? min(4095, sp) : static_cast<int>(4096.0 * 1.2 * g / (1.2 * g + left));
