@@ -276,6 +276,10 @@ typedef struct preft_plan preft_plan_t;
 preft_plan_t* preft_plan_create(const preft_meta_t* meta);
 void preft_plan_destroy(preft_plan_t* plan);
 int preft_plan_set_slot_split(preft_plan_t* plan, int32_t slot_split);
+/* expected selected rows per step: the K2 launch shape (team size) of every
+ * later run; a plan created before its meta's first build would otherwise
+ * keep the hint 0 (one-warp teams).  Never affects results. */
+int preft_plan_set_rows_hint(preft_plan_t* plan, int32_t rows_hint);
 int preft_plan_add_lora(preft_plan_t* plan, const void* x, int64_t ldx, int32_t m,
                         const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
                         int32_t dtype, int32_t tag);

@@ -174,6 +174,7 @@ SIGNATURES = {
     "preft_plan_create": (ctypes.c_void_p, [ctypes.POINTER(PreftMeta)]),
     "preft_plan_destroy": (None, [ctypes.c_void_p]),
     "preft_plan_set_slot_split": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "preft_plan_set_rows_hint": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "preft_plan_add_lora": (
         ctypes.c_int,
         [

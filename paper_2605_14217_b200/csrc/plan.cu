@@ -71,6 +71,12 @@ int preft_plan_set_slot_split(preft_plan* p, int32_t split) {
     return PREFT_OK;
 }
 
+int preft_plan_set_rows_hint(preft_plan* p, int32_t rows) {
+    if (!p || rows < 0) return PREFT_ERR_STATE;
+    p->meta.rows_hint = rows;
+    return PREFT_OK;
+}
+
 int preft_plan_add_lora(preft_plan* p, const void* x, int64_t ldx, int32_t m, const preft_lora_site_t* sites,
                         int32_t nsites, int32_t r_max, int32_t dtype, int32_t tag) {
     if (!p || !sites || nsites < 1 || nsites > 3) return PREFT_ERR_SHAPE;

@@ -12,6 +12,7 @@
 // used for the shrink and updated in registers for the expand, so h moves
 // HBM->SM->HBM exactly once — the algorithmic minimum 2*d*e bytes per token.
 // Wider rows re-read h for the expand (an L1/L2 hit in practice).
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -199,30 +200,31 @@ bool reft_res_eligible(int d, int r);
 // PREFT_REFT_COLAUNCH=0 disables, PREFT_REFT_COSPLIT=<fraction*4096 for the
 // parked kernel> overrides the split.
 struct CoStreams {
-    int device = -1;
     cudaStream_t aux = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
-static CoStreams g_co[16];
-
+// one aux stream + fork/join pair per (device, caller stream): two host
+// threads co-launching on different streams never share a fork event
+static std::map<std::pair<int, cudaStream_t>, CoStreams> g_co;
+// held from the fork record to the join wait, so no other co-launch can
+// re-record this pair's events in between
 static std::mutex g_co_mu;
 
-static CoStreams* co_streams(cudaStream_t stream) {
+static CoStreams* co_streams_locked(cudaStream_t stream) {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
-    std::lock_guard<std::mutex> lk(g_co_mu);
-    CoStreams& c = g_co[dev];
-    if (c.device < 0) {
-        // creating streams/events is not allowed while a capture is open: the
-        // first co-launch must run eagerly (a warm-up); until then, one kernel
-        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-        if (cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-        if (cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-        if (cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-        c.device = dev;
-    }
-    return &c;
+    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+    auto key = std::make_pair(dev, stream);
+    auto it = g_co.find(key);
+    if (it != g_co.end()) return &it->second;
+    // creating streams/events is not allowed while a capture is open: the
+    // first co-launch on a stream must run eagerly (a warm-up); until then, one kernel
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+    CoStreams c;
+    if (cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    if (cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+    return &(g_co[key] = c);
 }
 
 static int colaunch_split() {
@@ -245,7 +247,8 @@ static int reft_colaunch(const preft_meta_t* meta, void* h, long long rows, long
     const int g = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms, 0, 4096, true);
     const int left = num_sms - g;  // (a dry run returns the grid; error codes are < 32)
     if (g < 32 || left < 2) return PREFT_ERR_SHAPE;
-    CoStreams* c = co_streams(stream);
+    std::lock_guard<std::mutex> lk(g_co_mu);
+    CoStreams* c = co_streams_locked(stream);
     if (!c) return PREFT_ERR_SHAPE;
     // per-SM rate of the parked kernel ~1.2x the streaming kernel's (no L2 re-read misses)
     const int f = sp > 0 ? min(4095, sp) : static_cast<int>(4096.0 * 1.2 * g / (1.2 * g + left));
@@ -257,6 +260,10 @@ static int reft_colaunch(const preft_meta_t* meta, void* h, long long rows, long
     cudaEventRecord(c->join, c->aux);
     cudaStreamWaitEvent(stream, c->join, 0);
     if (rc == PREFT_OK) rc = rc2;
+    // once a half may have launched, a failure must not read as "ineligible"
+    // (PREFT_ERR_SHAPE): the caller would re-run the whole unit list and
+    // apply the delta twice to the units that did run
+    if (rc == PREFT_ERR_SHAPE) rc = PREFT_ERR_CONFIG;
     return rc;
 }
 

@@ -23,9 +23,28 @@ import torch
 from . import _lib
 from .adapters import PositionSchedule
 from .batch import ForwardBatch, Phase, mask_uniform
-from .errors import BatchError, InfeasibleBatchError
+from .errors import BatchError, ConfigError, InfeasibleBatchError, StateError
 
-__all__ = ["BatchMeta", "default_meta", "pack_entries"]
+__all__ = ["BatchMeta", "default_meta", "pack_entries", "validate_arrays"]
+
+
+def validate_arrays(qsl: np.ndarray, slots: np.ndarray, flags: np.ndarray) -> None:
+    """Host check of raw K1 arrays, the same rules K1 enforces on the device
+    (query_start_loc a strictly increasing prefix sum from 0, model.py:250-258;
+    one slot and one flag word per entry; known flag bits only)."""
+    qsl = np.asarray(qsl)
+    E = len(slots)
+    if qsl.ndim != 1 or len(qsl) != E + 1 or len(flags) != E:
+        raise BatchError(f"query_start_loc has {len(qsl)} offsets, slots {E}, flags {len(flags)}")
+    if int(qsl[0]) != 0:
+        raise BatchError("query_start_loc must start at 0")
+    if E and not bool(np.all(np.diff(qsl.astype(np.int64)) > 0)):
+        raise BatchError("query_start_loc must be strictly increasing (every entry has >= 1 token)")
+    fl = np.asarray(flags)
+    if E and int(np.bitwise_or.reduce(fl.astype(np.int64))) & ~(_lib.ENTRY_DECODE | _lib.ENTRY_ALL_POSITIONS):
+        raise BatchError("unknown entry flag bits")
+    if E and int(np.min(np.asarray(slots))) < -1:
+        raise BatchError("slot must be >= 0, or -1 for an adapter-less entry")
 
 
 def pack_entries(batch: ForwardBatch, slot_of: Mapping[int, int]) -> tuple[np.ndarray, np.ndarray, np.ndarray]:
@@ -104,6 +123,10 @@ class BatchMeta:
         self.E = 0
         self.T = 0
         self.uniform: bool | None = None
+        # slot_split in force when K1 last ran: K1 bakes the LoRA/ReFT token
+        # split into counters[SPLIT], so every launch that consumes this
+        # metadata must use a pool with the same split (require_split)
+        self.built_split: int | None = None
 
     @property
     def h2d_bytes(self) -> int:
@@ -113,18 +136,38 @@ class BatchMeta:
         return n_entries <= self.E_cap and n_tokens <= self.T_cap
 
     # ------------------------------------------------------------ build
-    def build(self, batch: ForwardBatch, slot_of: Mapping[int, int], stream: torch.cuda.Stream | None = None):
-        """Stage a ForwardBatch and launch K1 on `stream` (default: current)."""
+    def build(self, batch: ForwardBatch, slot_of: Mapping[int, int], stream: torch.cuda.Stream | None = None,
+              slot_split: int | None = None):
+        """Stage a ForwardBatch and launch K1 on `stream` (default: current).
+        `slot_split`: the pool's first ReFT slot (AdapterPool.slot_split)."""
         qsl, slots, flags = pack_entries(batch, slot_of)
         self.uniform = mask_uniform(batch)
-        return self.build_arrays(qsl, slots, flags, stream)
+        return self.build_arrays(qsl, slots, flags, stream, slot_split=slot_split)
 
     def set_slot_split(self, split: int) -> None:
-        """First ReFT-class slot (AdapterPool.slot_split); LoRA slots lie below it."""
+        """First ReFT-class slot (AdapterPool.slot_split) for the NEXT K1 run;
+        LoRA slots lie below it.  Changing it after a build does not re-split
+        the built metadata (require_split catches the mismatch)."""
         self.c.slot_split = int(split)
 
-    def build_arrays(self, qsl: np.ndarray, slots: np.ndarray, flags: np.ndarray, stream=None):
-        """Stage raw int32 arrays (qsl[E+1], slot[E], flags[E]) and launch K1."""
+    def require_split(self, split: int) -> None:
+        """Raise unless K1 last ran with this slot split (pool.slot_split)."""
+        if self.built_split is None:
+            raise StateError("batch metadata has not been built (BatchMeta.build / build_arrays)")
+        if self.built_split != int(split) or int(self.c.slot_split) != self.built_split:
+            raise ConfigError(
+                f"batch metadata was built with slot_split {self.built_split}, the pool's is {split}: "
+                "rebuild it with slot_split=pool.slot_split (or pool.build_meta)"
+            )
+
+    def build_arrays(self, qsl: np.ndarray, slots: np.ndarray, flags: np.ndarray, stream=None,
+                     slot_split: int | None = None, validate: bool = True):
+        """Stage raw int32 arrays (qsl[E+1], slot[E], flags[E]) and launch K1.
+
+        With `validate` (the default) the arrays are checked on the host the
+        way make_batch checks a ForwardBatch (model.py:250-261): a malformed
+        batch raises BatchError here instead of reaching K1, whose device
+        error bits would otherwise only surface at the next check_errors()."""
         E = int(len(slots))
         T = int(qsl[-1]) if E else 0
         if E < 1:
@@ -133,6 +176,10 @@ class BatchMeta:
             raise InfeasibleBatchError(
                 f"batch of {E} entries / {T} tokens exceeds the workspace ({self.E_cap} / {self.T_cap})"
             )
+        if validate:
+            validate_arrays(qsl, slots, flags)
+        if slot_split is not None:
+            self.set_slot_split(slot_split)
         if self._staged is not None:
             self._staged.synchronize()  # never overwrite a pinned buffer still being copied
         h = self._host_np
@@ -150,6 +197,7 @@ class BatchMeta:
             self._staged = ev
         self.c.rows_hint = T  # launch-shape hint for K2 (team size); results never depend on it
         _lib.check(_lib.load().preft_meta_build(ctypes.byref(self.c), ctypes.c_void_p(s.cuda_stream)), "meta_build")
+        self.built_split = int(self.c.slot_split)
         self.E, self.T = E, T
         return self
 
@@ -157,6 +205,7 @@ class BatchMeta:
         """Re-run K1 on whatever is in `entries` (graph replay helper)."""
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         _lib.check(_lib.load().preft_meta_build(ctypes.byref(self.c), ctypes.c_void_p(s.cuda_stream)), "meta_build")
+        self.built_split = int(self.c.slot_split)
 
     # ------------------------------------------------------------ readback (syncs)
     def counters_host(self) -> np.ndarray:

@@ -69,6 +69,59 @@ def _check_act(t: torch.Tensor, name: str, width: int, rows: int, dtype: torch.d
         raise ShapeError(f"{name} has {t.shape[0]} rows, the batch has {rows} tokens")
 
 
+def lora_site_chunks(sites: Sequence[str], rank: int) -> list[tuple[int, int]]:
+    """Split a group of sites sharing x into launches the kernel accepts:
+    at most 3 sites and nsites * r_max <= 64 per launch (include/preft.h)."""
+    per = max(1, min(3, 64 // max(1, rank)))
+    return [(i, min(len(sites), i + per)) for i in range(0, len(sites), per)]
+
+
+def check_lora_group(ys, x, meta_rows: int, pool: AdapterPool, layer: int, sites: Sequence[str]) -> int:
+    """Shared validation of a LoRA group (ops and StepPlan); returns m."""
+    if not 1 <= len(sites) <= 3 or len(ys) != len(sites):
+        raise ShapeError("a LoRA group has 1 to 3 sites and one output per site")
+    if not isinstance(layer, (int, np.integer)) or not 0 <= layer < pool.n_layers:
+        raise ShapeError(f"layer {layer} out of range [0, {pool.n_layers})")
+    if not pool.lora_capacity:
+        raise ShapeError("the pool holds no LoRA adapters")
+    if pool.tp_size > 1:
+        raise ConfigError("a tensor-parallel pool shard needs tp.apply_lora_group_tp_ (shrink, all-reduce, expand)")
+    unknown = [s for s in sites if s not in pool.lora_sites]
+    if unknown:
+        raise ShapeError(f"unknown LoRA site(s) {unknown}; the pool has {sorted(pool.lora_sites)}")
+    ms = {pool.lora_sites[s][1] for s in sites}
+    if len(ms) != 1:
+        raise ShapeError(f"sites {tuple(sites)} do not share an input width")
+    m = ms.pop()
+    _check_act(x, "x", m, meta_rows, pool.dtype, pool.device)
+    for name, y in zip(sites, ys):
+        _check_act(y, f"y[{name}]", pool.lora_sites[name][0], meta_rows, pool.dtype, pool.device)
+    return m
+
+
+def check_reft(h, meta_rows: int, pool: AdapterPool, layer: int) -> None:
+    if not pool.reft_capacity:
+        raise ShapeError("the pool holds no ReFT adapters")
+    if not isinstance(layer, (int, np.integer)) or not 0 <= layer < pool.n_layers:
+        raise ShapeError(f"layer {layer} out of range [0, {pool.n_layers})")
+    _check_act(h, "h", pool.d_model, meta_rows, pool.dtype, pool.device)
+
+
+def lora_site_array(ys, pool: AdapterPool, layer: int, sites: Sequence[str]):
+    arr = (_lib.PreftLoraSite * 3)()
+    for i, (name, y) in enumerate(zip(sites, ys)):
+        arr[i].A = pool.lora_A[name][layer].data_ptr()
+        arr[i].Bt = pool.lora_Bt[name][layer].data_ptr()
+        arr[i].scale = pool.lora_scale[name][layer].data_ptr()
+        arr[i].bias = None
+        arr[i].y = y.data_ptr()
+        arr[i].ldy = row_stride(y)
+        arr[i].n = pool.lora_sites[name][0]
+        tc = pool.lora_Bt_tc.get(name)
+        arr[i].Bt_tc = tc[layer].data_ptr() if tc is not None else None
+    return arr
+
+
 def apply_lora_group_(
     ys: Sequence[torch.Tensor],
     x: torch.Tensor,
@@ -78,38 +131,21 @@ def apply_lora_group_(
     sites: Sequence[str],
     stream=None,
 ) -> Sequence[torch.Tensor]:
-    """y_s[rows] += s_a * (x[rows] A_s,a^T) B_s,a^T for 1-3 sites sharing x, in place."""
-    if not 1 <= len(sites) <= 3 or len(ys) != len(sites):
-        raise ShapeError("a LoRA group has 1 to 3 sites and one output per site")
-    if not 0 <= layer < pool.n_layers:
-        raise ShapeError(f"layer {layer} out of range")
-    if not pool.lora_capacity:
-        raise ShapeError("the pool holds no LoRA adapters")
-    if pool.tp_size > 1:
-        raise ConfigError("a tensor-parallel pool shard needs tp.apply_lora_group_tp_ (shrink, all-reduce, expand)")
-    ms = {pool.lora_sites[s][1] for s in sites}
-    if len(ms) != 1:
-        raise ShapeError(f"sites {tuple(sites)} do not share an input width")
-    m = ms.pop()
-    _check_act(x, "x", m, meta.T, pool.dtype, pool.device)
-    arr = (_lib.PreftLoraSite * 3)()
-    for i, (name, y) in enumerate(zip(sites, ys)):
-        n = pool.lora_sites[name][0]
-        _check_act(y, f"y[{name}]", n, meta.T, pool.dtype, pool.device)
-        arr[i].A = pool.lora_A[name][layer].data_ptr()
-        arr[i].Bt = pool.lora_Bt[name][layer].data_ptr()
-        arr[i].scale = pool.lora_scale[name][layer].data_ptr()
-        arr[i].bias = None
-        arr[i].y = y.data_ptr()
-        arr[i].ldy = row_stride(y)
-        arr[i].n = n
+    """y_s[rows] += s_a * (x[rows] A_s,a^T) B_s,a^T for 1-3 sites sharing x, in place.
+
+    Groups whose fused rank would exceed the kernel's 64 rank-r lanes
+    (e.g. rank-32 q/k/v) run as several launches over the same x."""
+    m = check_lora_group(ys, x, meta.T, pool, layer, sites)
     s = _stream(stream, pool.device)
-    meta.set_slot_split(pool.slot_split)
-    st = _lib.load().preft_lora_apply(
-        ctypes.byref(meta.c), ctypes.c_void_p(x.data_ptr()), row_stride(x), m, arr, len(sites), pool.lora_rank,
-        pool.dtype_code, ctypes.c_void_p(s.cuda_stream)
-    )
-    _lib.check(st, "lora_apply")
+    meta.require_split(pool.slot_split)
+    lib = _lib.load()
+    for lo, hi in lora_site_chunks(sites, pool.lora_rank):
+        arr = lora_site_array(ys[lo:hi], pool, layer, sites[lo:hi])
+        st = lib.preft_lora_apply(
+            ctypes.byref(meta.c), ctypes.c_void_p(x.data_ptr()), row_stride(x), m, arr, hi - lo, pool.lora_rank,
+            pool.dtype_code, ctypes.c_void_p(s.cuda_stream)
+        )
+        _lib.check(st, "lora_apply")
     return ys
 
 
@@ -122,13 +158,9 @@ def apply_lora_(y: torch.Tensor, x: torch.Tensor, meta: BatchMeta, pool: Adapter
 
 def apply_reft_(h: torch.Tensor, meta: BatchMeta, pool: AdapterPool, layer: int, stream=None) -> torch.Tensor:
     """ReFT residual hook (model.py:543-546): h[rows] += delta(h[rows]), in place."""
-    if not pool.reft_capacity:
-        raise ShapeError("the pool holds no ReFT adapters")
-    if not 0 <= layer < pool.n_layers:
-        raise ShapeError(f"layer {layer} out of range")
-    _check_act(h, "h", pool.d_model, meta.T, pool.dtype, pool.device)
+    check_reft(h, meta.T, pool, layer)
     s = _stream(stream, pool.device)
-    meta.set_slot_split(pool.slot_split)
+    meta.require_split(pool.slot_split)
     st = _lib.load().preft_reft_apply(
         ctypes.byref(meta.c), ctypes.c_void_p(h.data_ptr()), h.shape[0], row_stride(h), pool.d_model,
         ctypes.c_void_p(pool.reft_A[layer].data_ptr()), ctypes.c_void_p(pool.reft_B[layer].data_ptr()),
@@ -176,11 +208,11 @@ class _OneSlot:
 
 def _one_entry_meta(n_sel: int, total: int, device, split: int) -> BatchMeta:
     """Batch of `total` rows whose first `n_sel` rows carry slot 0."""
-    n_entries = 1 if n_sel == total else 2
+    n_entries = 1 if n_sel in (0, total) else 2
     meta = default_meta(n_entries, total, device)
-    if n_sel == total:
+    if n_sel in (0, total):
         qsl = np.array([0, total], dtype=np.int32)
-        slots = np.array([0], dtype=np.int32)
+        slots = np.array([0 if n_sel else -1], dtype=np.int32)
     else:
         qsl = np.array([0, n_sel, total], dtype=np.int32)
         slots = np.array([0, -1], dtype=np.int32)

@@ -19,14 +19,18 @@ import torch
 from . import _lib
 from .errors import ShapeError
 from .meta import BatchMeta
-from .ops import _check_act, row_stride
+from .ops import check_lora_group, check_reft, lora_site_array, lora_site_chunks, row_stride
 from .pool import AdapterPool
 
 __all__ = ["StepPlan"]
 
 
 class StepPlan:
-    def __init__(self, meta: BatchMeta, pool: AdapterPool, max_tokens: int | None = None):
+    def __init__(self, meta: BatchMeta, pool: AdapterPool, max_tokens: int | None = None,
+                 rows_hint: int | None = None):
+        """`rows_hint`: the expected selected-row count per step, which picks
+        the K2 team size baked into the launches (and into a captured graph);
+        default: the meta's last build, else `max_tokens`.  Never affects results."""
         self.lib = _lib.load()
         self.meta = meta
         self.pool = pool
@@ -36,8 +40,12 @@ class StepPlan:
         if not self.handle:
             raise ShapeError("could not create a step plan")
         self.lib.preft_plan_set_slot_split(self.handle, pool.slot_split)
+        self.rows_hint = 0
+        self.set_rows_hint(rows_hint if rows_hint is not None else (meta.c.rows_hint or self.rows))
+        self._fixed_hint = rows_hint is not None
         self._keep: list = []  # tensors the plan points into
         self.n_ops = 0
+        self.n_launches = 0
         self.graph: torch.cuda.CUDAGraph | None = None
 
     def __del__(self):
@@ -46,35 +54,28 @@ class StepPlan:
             self.lib.preft_plan_destroy(h)
             self.handle = None
 
+    def set_rows_hint(self, rows: int) -> None:
+        self.rows_hint = int(rows)
+        _lib.check(self.lib.preft_plan_set_rows_hint(self.handle, self.rows_hint), "plan_set_rows_hint")
+
     def add_lora_group(self, ys: Sequence[torch.Tensor], x: torch.Tensor, layer: int, sites: Sequence[str],
                        tag: int = -1) -> None:
+        """Same contract and checks as ops.apply_lora_group_ (a group too wide
+        for one launch becomes several)."""
         pool = self.pool
-        if not 1 <= len(sites) <= 3 or len(ys) != len(sites):
-            raise ShapeError("a LoRA group has 1 to 3 sites and one output per site")
-        m = pool.lora_sites[sites[0]][1]
-        if any(pool.lora_sites[s][1] != m for s in sites):
-            raise ShapeError(f"sites {tuple(sites)} do not share an input width")
-        _check_act(x, "x", m, self.rows, pool.dtype, pool.device)
-        arr = (_lib.PreftLoraSite * 3)()
-        for i, (name, y) in enumerate(zip(sites, ys)):
-            n = pool.lora_sites[name][0]
-            _check_act(y, f"y[{name}]", n, self.rows, pool.dtype, pool.device)
-            arr[i].A = pool.lora_A[name][layer].data_ptr()
-            arr[i].Bt = pool.lora_Bt[name][layer].data_ptr()
-            arr[i].scale = pool.lora_scale[name][layer].data_ptr()
-            arr[i].bias = None
-            arr[i].y = y.data_ptr()
-            arr[i].ldy = row_stride(y)
-            arr[i].n = n
-        st = self.lib.preft_plan_add_lora(self.handle, ctypes.c_void_p(x.data_ptr()), row_stride(x), m, arr,
-                                          len(sites), pool.lora_rank, pool.dtype_code, tag)
-        _lib.check(st, "plan_add_lora")
+        m = check_lora_group(ys, x, self.rows, pool, layer, sites)
+        for lo, hi in lora_site_chunks(sites, pool.lora_rank):
+            arr = lora_site_array(ys[lo:hi], pool, layer, sites[lo:hi])
+            st = self.lib.preft_plan_add_lora(self.handle, ctypes.c_void_p(x.data_ptr()), row_stride(x), m, arr,
+                                              hi - lo, pool.lora_rank, pool.dtype_code, tag)
+            _lib.check(st, "plan_add_lora")
+            self.n_launches += 1
         self._keep += [x, *ys]
         self.n_ops += 1
 
     def add_reft(self, h: torch.Tensor, layer: int, tag: int = -1) -> None:
         pool = self.pool
-        _check_act(h, "h", pool.d_model, self.rows, pool.dtype, pool.device)
+        check_reft(h, self.rows, pool, layer)
         st = self.lib.preft_plan_add_reft(
             self.handle, ctypes.c_void_p(h.data_ptr()), h.shape[0], row_stride(h), pool.d_model,
             ctypes.c_void_p(pool.reft_A[layer].data_ptr()), ctypes.c_void_p(pool.reft_B[layer].data_ptr()),
@@ -85,11 +86,13 @@ class StepPlan:
         _lib.check(st, "plan_add_reft")
         self._keep.append(h)
         self.n_ops += 1
+        self.n_launches += 1
 
     @property
     def launches_per_run(self) -> int:
-        """Kernels one run() launches: K1 (2) + one per op."""
-        return 2 + self.n_ops
+        """Kernels one run() launches: K1 (2) + one per site launch (the
+        co-launched ReFT pair counts once)."""
+        return 2 + self.n_launches
 
     def set_timing(self, tag: int, reserve_pairs: int) -> None:
         _lib.check(self.lib.preft_plan_set_timing(self.handle, tag, reserve_pairs), "plan_set_timing")
@@ -102,8 +105,17 @@ class StepPlan:
         return total.value, count.value
 
     def run(self, stream=None, run_meta: bool = True) -> None:
+        """Issue the step.  run_meta=True re-runs K1 (with the pool's slot
+        split) on the entries already staged in the meta; run_meta=False
+        trusts the caller's build, which must have used the pool's split."""
         s = stream if stream is not None else torch.cuda.current_stream(self.pool.device)
+        if not run_meta:
+            self.meta.require_split(self.pool.slot_split)
+        if not self._fixed_hint and self.meta.c.rows_hint > 0 and self.meta.c.rows_hint != self.rows_hint:
+            self.set_rows_hint(self.meta.c.rows_hint)
         _lib.check(self.lib.preft_plan_run(self.handle, int(run_meta), ctypes.c_void_p(s.cuda_stream)), "plan_run")
+        if run_meta:
+            self.meta.built_split = int(self.pool.slot_split)
 
     def capture(self, stream=None, run_meta: bool = True) -> torch.cuda.CUDAGraph:
         """Capture one run() into a CUDA graph (timing must be off).  With

@@ -105,6 +105,17 @@ class StepBatch:
     qsl: np.ndarray = field(repr=False, default=None)  # int32 [E+1]
     adapter_ids: list = field(repr=False, default=None)  # per entry, None = base
     decode_flags: np.ndarray = field(repr=False, default=None)  # int32 [E], 1 = decode
+    all_positions: np.ndarray = field(repr=False, default=None)  # int32 [E], 1 = ALL_POSITIONS adapter
+
+    def entry_flags(self) -> np.ndarray:
+        """K1 flag word per entry (PREFT_ENTRY_*), from the scheduler's own
+        schedule map, so the device mask always agrees with the workset."""
+        from . import _lib
+
+        f = self.decode_flags.astype(np.int32) * _lib.ENTRY_DECODE
+        if self.all_positions is not None:
+            f = f | (self.all_positions.astype(np.int32) * _lib.ENTRY_ALL_POSITIONS)
+        return f.astype(np.int32)
 
     @property
     def prefill_tokens(self) -> int:
@@ -193,8 +204,10 @@ class Scheduler:
         qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
         ids = [r.spec.adapter_id for r in decode_sched] + [r.spec.adapter_id for r, _ in prefill_sched]
         dec = np.array([1] * len(decode_sched) + [0] * len(prefill_sched), dtype=np.int32)
+        allp = np.array([a is not None and self._schedule_of(a) is PositionSchedule.ALL_POSITIONS for a in ids],
+                        dtype=np.int32)
         step = StepBatch(self.step_idx, [r.spec.request_id for r in decode_sched],
-                         [(r.spec.request_id, c) for r, c in prefill_sched], list(workset), qsl, ids, dec)
+                         [(r.spec.request_id, c) for r, c in prefill_sched], list(workset), qsl, ids, dec, allp)
         # progress (engine.py:436-465)
         for req, chunk in prefill_sched:
             req.prefill_pos += chunk
@@ -209,13 +222,14 @@ class ServingLoop:
     """Replays a Scheduler on the device: paging + K1 + every layer's adapter
     sites per step, on one stream, timed with CUDA events."""
 
-    def __init__(self, paged, meta, layer_ops: Callable[[object, int], None], n_layers: int,
-                 schedule_of: Callable[[int], PositionSchedule] | None = None):
+    def __init__(self, paged, meta, layer_ops: Callable[[object, int], None], n_layers: int):
+        """Entry flags come from each StepBatch (the Scheduler's schedule map),
+        so the loop cannot disagree with the scheduler about which decode
+        tokens an ALL_POSITIONS adapter covers (model.py:316)."""
         self.paged = paged  # paging.PagedAdapterPool
         self.meta = meta  # meta.BatchMeta sized for the step token budget
         self.layer_ops = layer_ops  # (stream, layer) -> launches every adapter site of one layer
         self.n_layers = n_layers
-        self._schedule_of = schedule_of
 
     def run(self, scheduler: Scheduler, max_steps: int | None = None, stream=None) -> dict:
         import torch
@@ -236,14 +250,9 @@ class ServingLoop:
                 if max_steps is not None and steps >= max_steps:
                     break
                 continue
-            flags = step.decode_flags * _lib.ENTRY_DECODE
-            if self._schedule_of is not None:
-                allp = [a is not None and self._schedule_of(a) is PositionSchedule.ALL_POSITIONS
-                        for a in step.adapter_ids]
-                flags = flags | (np.asarray(allp, dtype=np.int32) * _lib.ENTRY_ALL_POSITIONS)
-            slots = pool.entry_arrays(step.qsl, step.adapter_ids, flags.astype(np.int32))
-            self.meta.set_slot_split(pool.slot_split)
-            self.meta.build_arrays(step.qsl, slots, flags.astype(np.int32), stream=s)
+            flags = step.entry_flags()  # the scheduler's schedules: mask == workset by construction
+            slots = pool.entry_arrays(step.qsl, step.adapter_ids, flags)
+            self.meta.build_arrays(step.qsl, slots, flags, stream=s, slot_split=pool.slot_split)
             for layer in range(self.n_layers):
                 self.layer_ops(s, layer)
             steps += 1

@@ -172,7 +172,7 @@ def lora_shrink_tp_(ys, x, meta, pool, layer: int, sites: Sequence[str], workspa
     ldp = len(sites) * pool.lora_rank
     P = workspace.view(rows, ldp)
     s = stream if stream is not None else torch.cuda.current_stream(pool.device)
-    meta.set_slot_split(pool.slot_split)
+    meta.require_split(pool.slot_split)
     st = _lib.load().preft_lora_shrink(
         ctypes.byref(meta.c), ctypes.c_void_p(x.data_ptr() + shards[0].x_offset * x.element_size()), rows,
         row_stride(x), shards[0].m_loc, arr, len(sites), pool.lora_rank, pool.dtype_code,
@@ -190,7 +190,7 @@ def lora_expand_tp_(P, ys, x, meta, pool, layer: int, sites: Sequence[str], stre
 
     arr, _, rows = _site_array(ys, x, meta, pool, layer, sites)
     s = stream if stream is not None else torch.cuda.current_stream(pool.device)
-    meta.set_slot_split(pool.slot_split)
+    meta.require_split(pool.slot_split)
     st = _lib.load().preft_lora_expand(
         ctypes.byref(meta.c), ctypes.c_void_p(P.data_ptr()), P.shape[1], rows, arr, len(sites), pool.lora_rank,
         pool.dtype_code, ctypes.c_void_p(s.cuda_stream),

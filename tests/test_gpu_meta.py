@@ -85,7 +85,10 @@ def test_device_rejects_malformed_offsets(cuda_device):
     from paper_2605_14217_b200.meta import BatchMeta
 
     meta = BatchMeta(8, 64, device=cuda_device)
-    meta.build_arrays(np.array([0, 3, 3, 5], dtype=np.int32), np.zeros(3, np.int32), np.zeros(3, np.int32))
+    bad = (np.array([0, 3, 3, 5], dtype=np.int32), np.zeros(3, np.int32), np.zeros(3, np.int32))
+    with pytest.raises(BatchError):  # the host check (default) stops it before K1
+        meta.build_arrays(*bad)
+    meta.build_arrays(*bad, validate=False)  # the device check: K1's error bits
     with pytest.raises(BatchError):
         meta.check_errors()
     with pytest.raises(InfeasibleBatchError):

@@ -234,3 +234,27 @@ def test_adapter_directory_rejects_corruption(tmp_path):
         load_model_adapter(d)
     with pytest.raises(ShapeError):
         load_model_adapter(tmp_path / "missing")
+
+
+def test_lora_site_chunks_respect_kernel_limit():
+    """nsites * r_max <= 64 and <= 3 sites per launch (include/preft.h)."""
+    from paper_2605_14217_b200.ops import lora_site_chunks
+
+    sites = ("Wq", "Wk", "Wv")
+    assert lora_site_chunks(sites, 1) == [(0, 3)]
+    assert lora_site_chunks(sites, 16) == [(0, 3)]
+    assert lora_site_chunks(sites, 32) == [(0, 2), (2, 3)]
+    assert lora_site_chunks(sites, 64) == [(0, 1), (1, 2), (2, 3)]
+    assert lora_site_chunks(("Wgate", "Wup"), 64) == [(0, 1), (1, 2)]
+
+
+def test_validate_arrays_matches_make_batch_rules():
+    from paper_2605_14217_b200.errors import BatchError
+    from paper_2605_14217_b200.meta import validate_arrays
+
+    ok = (np.array([0, 2, 5], np.int32), np.array([0, -1], np.int32), np.array([1, 2], np.int32))
+    validate_arrays(*ok)
+    for bad in ((np.array([0, 2, 2], np.int32), ok[1], ok[2]), (np.array([1, 2, 5], np.int32), ok[1], ok[2]),
+                (ok[0], ok[1], np.array([0, 4], np.int32)), (ok[0], np.array([0, -3], np.int32), ok[2])):
+        with pytest.raises(BatchError):
+            validate_arrays(*bad)

@@ -119,3 +119,29 @@ def test_schedule_matches_live_reference(seed):
     assert rec["workset"] == [list(s.workset) for s in res.steps]
     assert rec["resident"] == [list(s.resident) for s in res.steps]
     assert rec["paged_in"] == [list(s.paged_in) for s in res.steps]
+
+
+def test_step_entry_flags_follow_the_scheduler_schedule():
+    """The K1 flags of a step come from the Scheduler's own schedule map, so
+    an ALL_POSITIONS adapter's decode tokens are both in the workset and
+    selected by the device mask (model.py:316)."""
+    from oracle import preft_oracle as O
+    from paper_2605_14217_b200 import _lib
+
+    wl = generate_workload(WorkloadConfig(40, 6, AdapterMix.UNIFORM, seed=2, l_max=48))
+    sched_of = {a: (PositionSchedule.ALL_POSITIONS if a % 2 else PositionSchedule.PREFILL_ONLY) for a in range(6)}
+    n_dec_selected = 0
+    for step in Scheduler(wl, ServeConfig(max_batch=8, max_gpu_adapters=6, step_token_budget=64),
+                          lambda a: sched_of[a]):
+        flags = step.entry_flags()
+        dec = (flags & _lib.ENTRY_DECODE) != 0
+        allp = (flags & _lib.ENTRY_ALL_POSITIONS) != 0
+        slots = np.array([-1 if a is None else a for a in step.adapter_ids], np.int32)
+        mask = O.position_mask(step.qsl, slots, dec, allp)
+        for i, a in enumerate(step.adapter_ids):
+            sel = bool(mask[step.qsl[i]])
+            assert sel == (a is not None and (not dec[i] or sched_of[a] is PositionSchedule.ALL_POSITIONS))
+            if sel:
+                assert a in step.workset  # every selected token's adapter is resident
+            n_dec_selected += int(sel and dec[i])
+    assert n_dec_selected > 0
