@@ -12,7 +12,6 @@
 // used for the shrink and updated in registers for the expand, so h moves
 // HBM->SM->HBM exactly once — the algorithmic minimum 2*d*e bytes per token.
 // Wider rows re-read h for the expand (an L1/L2 hit in practice).
-#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -200,31 +199,33 @@ bool reft_res_eligible(int d, int r);
 // PREFT_REFT_COLAUNCH=0 disables, PREFT_REFT_COSPLIT=<fraction*4096 for the
 // parked kernel> overrides the split.
 struct CoStreams {
+    int device = -1;
     cudaStream_t aux = nullptr;
     cudaEvent_t fork = nullptr, join = nullptr;
 };
-// one aux stream + fork/join pair per (device, caller stream): two host
-// threads co-launching on different streams never share a fork event
-static std::map<std::pair<int, cudaStream_t>, CoStreams> g_co;
-// held from the fork record to the join wait, so no other co-launch can
-// re-record this pair's events in between
+static CoStreams g_co[16];
+// held from the fork record to the join wait: two host threads co-launching
+// (on any streams) cannot interleave record(fork) / wait(aux, fork), so each
+// aux half always waits for its own caller stream's prior work.  One pair per
+// device (created at the first eager co-launch) keeps a later capture on any
+// stream able to fork.
 static std::mutex g_co_mu;
 
 static CoStreams* co_streams_locked(cudaStream_t stream) {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
-    auto key = std::make_pair(dev, stream);
-    auto it = g_co.find(key);
-    if (it != g_co.end()) return &it->second;
-    // creating streams/events is not allowed while a capture is open: the
-    // first co-launch on a stream must run eagerly (a warm-up); until then, one kernel
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
-    CoStreams c;
-    if (cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-    if (cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    if (cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
-    return &(g_co[key] = c);
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    CoStreams& c = g_co[dev];
+    if (c.device < 0) {
+        // creating streams/events is not allowed while a capture is open: the
+        // first co-launch must run eagerly (a warm-up); until then, one kernel
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+        if (cudaStreamCreateWithFlags(&c.aux, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&c.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        if (cudaEventCreateWithFlags(&c.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+        c.device = dev;
+    }
+    return &c;
 }
 
 static int colaunch_split() {

@@ -250,6 +250,77 @@ def gen_hooks(shuffle: bool):
     np.savez_compressed(OUT / f"hooks_config1_small{'_shuffled' if shuffle else ''}.npz", **out)
 
 
+CFG1_D = 4096
+
+
+def config1_entries(shuffle: bool):
+    """BASELINE configs[0] exactly (SURVEY 8(d) cfg 1): 32 decode entries
+    (PREFILL_ONLY adapters, unselected) then 32 prefill entries x 128 tokens;
+    prefill entry i -> adapter i: ids 0-15 DiReFT^P r=8 (residual site),
+    ids 16-31 LoRA^P r=1 (one 4096 -> 4096 site).  `shuffle` permutes the
+    entries with rng_from_seed(0, 7)."""
+    P = RA.PositionSchedule
+    entries = [RM.SeqEntry(100 + i, (1,), 129, RM.Phase.DECODE, adapter_id=i, schedule=P.PREFILL_ONLY)
+               for i in range(32)]
+    entries += [RM.SeqEntry(i, tuple(range(128)), 128, RM.Phase.PREFILL, adapter_id=i, schedule=P.PREFILL_ONLY)
+                for i in range(32)]
+    if shuffle:
+        order = rng_from_seed(0, 7).permutation(len(entries))
+        entries = [entries[j] for j in order]
+    return entries
+
+
+def config1_params():
+    """init_zero_delta(kind, r, dims, seed=a) then _perturbed_params(seed=a+1000, sigma=0.1) (model.py:383-397)."""
+    K = RA.AdapterKind
+    out = {}
+    for a in range(32):
+        kind, r, dims = (K.DIREFT, 8, (CFG1_D,)) if a < 16 else (K.LORA, 1, (CFG1_D, CFG1_D))
+        out[a] = RM._perturbed_params(RA.init_zero_delta(kind, r, dims, a), a + 1000, 0.1)
+    return out
+
+
+def gen_config1_full(shuffle: bool):
+    """BASELINE configs[0] at its stated size through the reference's own hook
+    code: LoRA via _project (model.py:442-452, with W = 0 so its output is the
+    delta alone), ReFT via the residual hook (model.py:543-546).  Inputs come
+    from rng_from_seed(0, 1) in the order x, h; the full outputs are pinned by
+    sha256 and a sample of rows is stored (the arrays are 135 MB each)."""
+    K = RA.AdapterKind
+    d = CFG1_D
+    entries = config1_entries(shuffle)
+    params = config1_params()
+    b = RM.make_batch(entries)
+    T = b.total_tokens
+    mask = RM.compute_position_mask(b).values
+    rng = rng_from_seed(0, 1)
+    x = rng.normal(size=(T, d))
+    h = rng.normal(size=(T, d))
+    W0 = np.zeros((d, d))
+    delta = np.zeros((T, d))
+    h_ref = h.copy()
+    for i, e in enumerate(entries):
+        sp = b.span(i)
+        rows = mask[sp]
+        p = params[e.adapter_id]
+        if p.kind is K.LORA:
+            delta[sp] = RM._project(x[sp], W0, p, rows)
+        elif rows.any():
+            blk = h_ref[sp]
+            blk[rows] += RA.delta_for_rows(p, blk[rows])
+            h_ref[sp] = blk
+    sel = np.flatnonzero(mask)
+    pick = np.sort(np.concatenate([rng_from_seed(0, 9).choice(sel, size=24, replace=False),
+                                   np.flatnonzero(~mask)[:4]]))
+    a, dec, allp, plen = entry_arrays(entries)
+    out = dict(qsl=np.asarray(b.query_start_loc), adapter=a, is_decode=dec, all_pos=allp, prompt_len=plen,
+               mask=mask, rows=pick, delta_rows=delta[pick], h_rows=h_ref[pick],
+               delta_sha256=np.array(hashlib.sha256(np.ascontiguousarray(delta).tobytes()).hexdigest()),
+               h_sha256=np.array(hashlib.sha256(np.ascontiguousarray(h_ref).tobytes()).hexdigest()),
+               d=np.array(d))
+    np.savez_compressed(OUT / f"config1_full{'_shuffled' if shuffle else ''}.npz", **out)
+
+
 def gen_init_and_io():
     K, P = RA.AdapterKind, RA.PositionSchedule
     out = {}
@@ -306,6 +377,8 @@ def main():
     nm = gen_masked()
     gen_hooks(False)
     gen_hooks(True)
+    gen_config1_full(False)
+    gen_config1_full(True)
     gen_init_and_io()
     (OUT / "REFERENCE_DIGEST.txt").write_text(
         f"prefillsim {prefillsim.__version__}\nsha256(adapters.py+model.py+linalg.py) {ref_digest()}\n"

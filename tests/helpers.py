@@ -107,3 +107,38 @@ def check_close(out, base, ref, mode: str, what: str = ""):
         f"{what}: delta mismatch at {int(bad.sum())} elements, worst "
         f"{np.max(np.abs(d_out - d_ref)):.3e} vs delta scale {dscale:.3e}"
     )
+
+
+# ---------------------------------------------------------------- BASELINE config 1 at its stated size
+
+CFG1_D = 4096
+
+
+def config1_full(shuffle: bool):
+    """BASELINE configs[0] exactly, regenerated with this package's restated
+    seeded constructors (bit-identical to the reference's, pinned by
+    test_host_api / test_reference_live) in the order make_golden.py
+    gen_config1_full uses: entries, adapters (init_zero_delta + perturbation,
+    sigma 0.1), then x, h from rng_from_seed(0, 1).  Returns the golden file's
+    arrays too (sampled reference rows + sha256 of the full outputs)."""
+    from paper_2605_14217_b200.adapters import AdapterKind, init_zero_delta
+    from paper_2605_14217_b200.batch import _perturbed_params
+    from paper_2605_14217_b200.linalg import rng_from_seed
+
+    g = load(f"config1_full{'_shuffled' if shuffle else ''}.npz")
+    d = CFG1_D
+    params = {}
+    for a in range(32):
+        kind, r, dims = (AdapterKind.DIREFT, 8, (d,)) if a < 16 else (AdapterKind.LORA, 1, (d, d))
+        params[a] = _perturbed_params(init_zero_delta(kind, r, dims, a), a + 1000, 0.1)
+    T = int(g["qsl"][-1])
+    rng = rng_from_seed(0, 1)
+    x = rng.normal(size=(T, d))
+    h = rng.normal(size=(T, d))
+    return g, params, x, h
+
+
+def oracle_params(p) -> dict:
+    """Oracle kwargs of an AdapterParams bundle (its own float64 operands)."""
+    kw = {k: getattr(p, k) for k in ("A", "B", "b", "R", "W") if getattr(p, k) is not None}
+    return dict(kind=p.kind.value, s=float(p.prefactor), **kw)

@@ -112,16 +112,19 @@ def test_split_tc_forced_rejects_ineligible_shapes(cuda_device):
         lib.preft_set_split_variant(-1)
 
 
-@pytest.mark.parametrize("tp", [2, 4])
-def test_tensor_parallel_emulated_on_one_gpu(cuda_device, tp):
+@pytest.mark.parametrize("tp,widths", [(2, (1024, 256, 2048)), (4, (1024, 256, 2048)), (8, (8192, 1024, 28672))])
+def test_tensor_parallel_emulated_on_one_gpu(cuda_device, tp, widths):
     """tp shards of one pool: every rank's shrink partials summed (what the
     NCCL all-reduce does), every rank expands into its slice; the assembled
-    result equals the unsharded oracle for column- and row-parallel sites."""
+    result equals the unsharded oracle for column- and row-parallel sites.
+    tp = 8 runs BASELINE config 4's own per-rank shapes: Llama-3.1-70B sites
+    split 8 ways (k/v n_loc = 128, the tcgen05 expand's minimum width; Wdown
+    m_loc = 3584)."""
     from paper_2605_14217_b200.meta import BatchMeta
     from paper_2605_14217_b200.tp import SplitWorkspace, lora_expand_tp_, lora_shrink_tp_
 
     rng = np.random.default_rng(tp)
-    sites = _sites(1024, 256, 2048)
+    sites = _sites(*widths)
     full = _pool(cuda_device, sites, 16, torch.bfloat16)
     shards = [_pool(cuda_device, sites, 16, torch.bfloat16, tp_rank=r, tp_size=tp) for r in range(tp)]
     ids = [100 + a for a in range(5)]
@@ -137,6 +140,8 @@ def test_tensor_parallel_emulated_on_one_gpu(cuda_device, tp):
     for p, m in zip(shards, metas):
         slots = U.stage(m, p, qsl, eids, flags)
     mask = U.oracle_mask(qsl, slots, flags)
+    if tp == 8:
+        assert shards[0].lora_shard["Wk"].n_loc == 128 and shards[0].lora_shard["Wdown"].m_loc == 3584
     for group in GROUPS:
         sh = [p.lora_shard[s] for s in group for p in shards[:1]][0]
         n_full = [sites[s][0] for s in group]

@@ -98,3 +98,24 @@ def test_forward_hooks_match_reference(name):
     # decode / adapter-less rows untouched, bit for bit
     assert np.array_equal(y[~mask], g["y_base"][~mask])
     assert np.array_equal(h[~mask], g["h"][~mask])
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_config1_full_size_bit_exact_against_reference(shuffle):
+    """BASELINE configs[0] at its stated size (d = 4096, 32 decode + 32 x 128
+    prefill, 16 DiReFT^P r8 + 16 LoRA^P r1): the oracle reproduces the
+    reference's hook outputs BIT FOR BIT (sha256 of the full f64 arrays, made
+    by make_golden.gen_config1_full through _project / the residual hook)."""
+    import hashlib
+
+    g, params, x, h = helpers.config1_full(shuffle)
+    qsl, ad = g["qsl"], g["adapter"]
+    mask = O.position_mask(qsl, ad, g["is_decode"], g["all_pos"])
+    assert np.array_equal(mask, g["mask"]) and int(mask.sum()) == 4096 and len(mask) == 4128
+    lora = {a: helpers.oracle_params(p) for a, p in params.items() if a >= 16}
+    reft = {a: helpers.oracle_params(p) for a, p in params.items() if a < 16}
+    delta = O.lora_hook(np.zeros_like(x), x, qsl, mask, np.where(ad >= 16, ad, -1), lora)
+    h_out = O.reft_hook(h, qsl, mask, np.where((ad >= 0) & (ad < 16), ad, -1), reft)
+    assert hashlib.sha256(delta.tobytes()).hexdigest() == str(g["delta_sha256"])
+    assert hashlib.sha256(h_out.tobytes()).hexdigest() == str(g["h_sha256"])
+    assert np.array_equal(delta[g["rows"]], g["delta_rows"]) and np.array_equal(h_out[g["rows"]], g["h_rows"])
