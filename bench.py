@@ -19,10 +19,14 @@ metric through the reference-shaped host-buffer path: every step uploads the
 entries and every layer's site activations from pinned host memory and
 reads every updated output back.
 
---impl reference times the reference's CPU implementation of the same path
-(oracle/preft_oracle.py: the float64 numpy restatement of delta_for_rows /
-the forward_chunk hooks, the reference itself being pure Python that cannot
-travel to the GPU box) on all host cores, on rank 0 only.
+Every timed line is followed (outside the timed region) by a parity check of
+sampled rows against the CPU oracle on the device's own operands
+(`"parity": {...}`); a failed check makes the line say so.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run
+(one NCCL rank per GPU).  --impl reference times the UNMODIFIED reference
+(prefillsim, installed into oracle/_ref by oracle/build_ref.py) on all host
+cores over the same cfg2 batch, rank 0 only.
 """
 
 from __future__ import annotations
@@ -30,6 +34,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -50,7 +55,7 @@ N_LAYERS = 32
 SEED = 0
 
 
-def parse():
+def parse(argv=None):
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
@@ -63,8 +68,13 @@ def parse():
     p.add_argument("--no-punica-step", action="store_true")
     p.add_argument("--no-secondary", action="store_true", help="skip the config-1/3/5 secondary lines")
     p.add_argument("--cpu-seconds", type=float, default=10.0, help="bounded CPU baseline sample length")
-    p.add_argument("--ref-requests", type=int, default=4, help="reference arm: requests per worker per step")
-    return p.parse_args()
+    p.add_argument("--ref-cores", type=int, default=0, help="reference arm: processes (0 = every host core)")
+    p.add_argument("--no-parity", action="store_true", help="skip the post-timing parity checks")
+    p.add_argument("--only", default="", help="comma list of secondary lines to run alone: "
+                   "cfg1,cfg3,cfg5,cfg5s,cfg4,serving,punica,lora16 (skips the headline)")
+    p.add_argument("--dry-run", action="store_true",
+                   help="CPU/gloo launcher check: routing + collectives + the JSON line, no kernels")
+    return p.parse_args(argv)
 
 
 # ---------------------------------------------------------------- workload
@@ -166,11 +176,9 @@ def measured_peak_gbs() -> tuple[float, str]:
 def group_bytes(shape, group, n_tokens: int, distinct: int, rank: int = RANK, elem: int = 2) -> int:
     """Algorithmic bytes of one fused launch: x read once,
     every y read + written, each distinct adapter's A/Bt rows once."""
-    dims = shape.site_dims()
-    m = dims[group[0]][1]
-    act = n_tokens * elem * (m + 2 * sum(dims[s][0] for s in group))
-    wts = distinct * elem * rank * sum(m + dims[s][0] for s in group)
-    return act + wts
+    from paper_2605_14217_b200 import costs
+
+    return costs.lora_group_bytes(shape.site_dims(), group, n_tokens, distinct, rank, elem)
 
 
 def ncu_traffic(kernel_hint: str):
@@ -189,6 +197,26 @@ def ncu_traffic(kernel_hint: str):
 # ---------------------------------------------------------------- distributed
 
 
+def _free_port() -> int:
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def maybe_self_launch(args) -> None:
+    """`bench.py --gpus N` outside torchrun: re-run this script under
+    torch.distributed.run with N ranks (one per GPU, NCCL; gloo for
+    --dry-run) and exit with its status.  Rank 0 prints the JSON line."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+           *sys.argv[1:]]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "4"))
+    sys.stdout.flush()
+    sys.exit(subprocess.call(cmd, env=env))
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -196,15 +224,29 @@ def dist_setup(args):
     return world, rank, local
 
 
-def dist_init(world, local):
+_BACKEND = {"name": None}
+
+
+def dist_init(world, local, backend: str = "nccl"):
     import torch
 
-    torch.cuda.set_device(local)
+    if backend == "nccl":
+        torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+        _BACKEND["name"] = backend
+
+
+def _reduce_device():
+    import torch
+
+    return torch.device("cuda") if _BACKEND["name"] == "nccl" else torch.device("cpu")
 
 
 def barrier(world):
@@ -220,7 +262,7 @@ def all_max(value: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=_reduce_device())
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -231,15 +273,182 @@ def all_sum(value: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([value], dtype=torch.float64, device="cuda")
+    t = torch.tensor([value], dtype=torch.float64, device=_reduce_device())
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def all_gather_floats(value: float, world: int) -> list[float]:
+    if world == 1:
+        return [value]
+    import torch
+    import torch.distributed as dist
+
+    t = torch.zeros(world, dtype=torch.float64, device=_reduce_device())
+    t[int(os.environ.get("RANK", "0"))] = value
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [float(v) for v in t.tolist()]
+
+
+# ---------------------------------------------------------------- parity (checker, never timed)
+
+
+def _np(t):
+    import torch
+
+    return t.detach().to(torch.float64).cpu().numpy()
+
+
+def _row_entries(qsl: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    return np.searchsorted(np.asarray(qsl), rows, side="right") - 1
+
+
+def sample_rows(mask: np.ndarray, qsl, k: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """(selected rows, unselected rows): k selected rows spread over the
+    entries (first/last rows of the longest entries included) + up to 8
+    unselected ones."""
+    rng = np.random.default_rng(seed)
+    sel = np.flatnonzero(mask)
+    uns = np.flatnonzero(~mask)
+    pick = rng.choice(sel, size=min(k, len(sel)), replace=False) if len(sel) else sel
+    lens = np.diff(np.asarray(qsl))
+    edge = []
+    for e in np.argsort(-lens)[:2]:
+        b, en = int(qsl[e]), int(qsl[e + 1])
+        edge += [b, en - 1] if mask[b] else []
+    pick = np.unique(np.concatenate([pick, np.asarray(edge, dtype=np.int64)])).astype(np.int64)
+    u = rng.choice(uns, size=min(8, len(uns)), replace=False) if len(uns) else uns
+    return pick, np.sort(u).astype(np.int64)
+
+
+def _verdict(errs: list[float], n_rows: int, tol: float, extra: dict | None = None) -> dict:
+    worst = max(errs) if errs else 0.0
+    out = {"status": "pass" if worst <= tol else "FAIL", "rows_checked": int(n_rows),
+           "max_rel_err": float(f"{worst:.3e}"), "tol": tol,
+           "vs": "oracle/preft_oracle.py (float64) on the device's own operands, sampled rows"}
+    if extra:
+        out.update(extra)
+    return out
+
+
+def _rel(out: np.ndarray, ref: np.ndarray) -> float:
+    den = float(np.max(np.abs(ref))) if ref.size else 0.0
+    return float(np.max(np.abs(out - ref))) / den if den > 0 else float(np.max(np.abs(out - ref), initial=0.0))
+
+
+def lora_rows_delta(pool, layers, site: str, row_slots: np.ndarray, x_rows: np.ndarray, shard=None) -> np.ndarray:
+    """sum over `layers` of the LoRA delta of each row (adapters.py:284-288),
+    with the pool's stored operands (for a TP shard: its own A / B slices and
+    the matching slice of x)."""
+    import torch
+
+    from oracle import preft_oracle as O
+
+    idx = torch.as_tensor(row_slots, device=pool.device, dtype=torch.long)
+    n = pool.lora_shard[site].n_loc if shard else pool.lora_sites[site][0]
+    out = np.zeros((len(row_slots), n))
+    for L in layers:
+        A = _np(pool.lora_A[site][L].index_select(0, idx))
+        Bt = _np(pool.lora_Bt[site][L].index_select(0, idx))
+        sc = _np(pool.lora_scale[site][L].index_select(0, idx))
+        for j in range(len(row_slots)):
+            out[j] += O.delta_rows("lora", float(sc[j]), x_rows[j:j + 1], A=A[j], B=Bt[j].T)[0]
+    return out
+
+
+def check_lora_accumulated(pool, meta, qsl, slots, groups_acts, snapshot, layers, k=48, seed=0,
+                           n_updates: int = 1) -> dict:
+    """After one more run of a timed plan: y_s[rows] must equal y0 + the
+    sum over `layers` of every site's delta (oracle), unselected rows
+    untouched bit for bit.  `groups_acts` {group: (x, ys)}, `snapshot`
+    {group: [y0 per site]} taken just before the run."""
+    import torch
+
+    mask = meta.mask_host()
+    sel, uns = sample_rows(mask, qsl, k, seed)
+    ent = _row_entries(qsl, sel)
+    row_slots = np.asarray(slots)[ent]
+    errs, dlt = [], []
+    for group, (x, ys) in groups_acts.items():
+        xr = _np(x[torch.as_tensor(sel, device=x.device)])
+        for s, y, y0 in zip(group, ys, snapshot[group]):
+            if len(uns):
+                ui = torch.as_tensor(uns, device=y.device)
+                if not torch.equal(y[ui], y0[ui]):
+                    return _verdict([float("inf")], len(sel), 2e-2, {"error": f"{s}: unselected rows modified"})
+            si = torch.as_tensor(sel, device=y.device)
+            out, base = _np(y[si]), _np(y0[si])
+            d_ref = lora_rows_delta(pool, layers, s, row_slots, xr)
+            errs.append(_rel(out, base + d_ref))
+            dlt.append(_rel(out - base, d_ref))
+    return _verdict(errs, len(sel), 2e-2, {"delta_rel_err": float(f"{max(dlt):.3e}"), "layers": len(layers),
+                                           "bf16_roundings_per_row": n_updates})
+
+
+def check_reft_chain(pool, meta, qsl, slots, h, h0_rows, sel, layers, kind_label: str) -> dict:
+    """A ReFT plan applies the residual edit layer after layer to the same h
+    (model.py:543-546 once per layer): the oracle replays the chain on the
+    sampled rows in float64, rounding to bf16 between layers as the stored
+    activation is."""
+    import torch
+
+    from oracle import preft_oracle as O
+
+    ent = _row_entries(qsl, sel)
+    js = np.asarray(slots)[ent] - pool.slot_split
+    idx = torch.as_tensor(js, device=pool.device, dtype=torch.long)
+    ref = h0_rows.copy()
+    for L in layers:
+        A = _np(pool.reft_A[L].index_select(0, idx))
+        B = _np(pool.reft_B[L].index_select(0, idx))
+        b = _np(pool.reft_bias[L].index_select(0, idx))
+        sc = _np(pool.reft_scale[L].index_select(0, idx))
+        for j in range(len(sel)):
+            ref[j] = ref[j] + O.delta_rows("direft", float(sc[j]), ref[j:j + 1], A=A[j], B=B[j], b=b[j])[0]
+        ref = torch.from_numpy(ref).to(torch.bfloat16).double().numpy()
+    out = _np(h[torch.as_tensor(sel, device=h.device)])
+    return _verdict([_rel(out, ref)], len(sel), 2e-2, {"layers": len(layers), "chain": kind_label})
+
+
+def check_reft_single(pool, meta, qsl, slots, h, layer: int, k=48, seed=0) -> dict:
+    """One apply_reft_ launch on a copy of h: the delta itself to tolerance."""
+    import torch
+
+    from oracle import preft_oracle as O
+    from paper_2605_14217_b200.ops import apply_reft_
+
+    mask = meta.mask_host()
+    sel, uns = sample_rows(mask, qsl, k, seed)
+    hc = h.clone()
+    apply_reft_(hc, meta, pool, layer)
+    torch.cuda.synchronize()
+    si = torch.as_tensor(sel, device=h.device)
+    base, out = _np(h[si]), _np(hc[si])
+    if len(uns):
+        ui = torch.as_tensor(uns, device=h.device)
+        if not torch.equal(hc[ui], h[ui]):
+            return _verdict([float("inf")], len(sel), 2e-2, {"error": "unselected rows modified"})
+    js = np.asarray(slots)[_row_entries(qsl, sel)] - pool.slot_split
+    d_ref = np.zeros_like(base)
+    for j in range(len(sel)):
+        jj = int(js[j])
+        d_ref[j] = O.delta_rows("direft", float(_np(pool.reft_scale[layer][jj])), base[j:j + 1],
+                                A=_np(pool.reft_A[layer][jj]), B=_np(pool.reft_B[layer][jj]),
+                                b=_np(pool.reft_bias[layer][jj]))[0]
+    # the stored output adds one bf16 rounding of |h| on top of the delta
+    ulp = float(np.max(np.abs(base + d_ref))) * 2.0 ** -8
+    err = float(np.max(np.abs((out - base) - d_ref)))
+    rel = err / max(float(np.max(np.abs(d_ref))), 1e-30)
+    ok = err <= 2e-2 * float(np.max(np.abs(d_ref))) + ulp
+    return {"status": "pass" if ok else "FAIL", "rows_checked": int(len(sel)), "delta_rel_err": float(f"{rel:.3e}"),
+            "tol": "2e-2 x max|delta| + 1 bf16 ulp of the output", "layer": layer,
+            "vs": "oracle/preft_oracle.py (float64) on the device's own operands, sampled rows"}
 
 
 # ---------------------------------------------------------------- our arm
 
 
-def build_step(args, rank, world, device, n_prefill, n_decode, seed=SEED):
+def build_step(args, rank, world, device, n_prefill, n_decode, seed=SEED, lora_rank: int = RANK):
     import torch
 
     from paper_2605_14217_b200 import AdapterKind, shapes
@@ -250,13 +459,12 @@ def build_step(args, rank, world, device, n_prefill, n_decode, seed=SEED):
     shape = shapes.LLAMA_8B
     qsl, ids, flags, lens, owned = step_entries(rank, world, n_prefill, n_decode, seed)
     pool = AdapterPool(N_LAYERS, shape.d_model, lora_sites=shape.site_dims(), lora_capacity=len(owned),
-                       lora_rank=RANK, dtype=torch.bfloat16, device=device)
-    pool.fill_synthetic_(0, AdapterKind.LORA, RANK, seed=seed + 17 * rank, sigma=0.01, ids=owned)
+                       lora_rank=lora_rank, dtype=torch.bfloat16, device=device)
+    pool.fill_synthetic_(0, AdapterKind.LORA, lora_rank, seed=seed + 17 * rank, sigma=0.01, ids=owned)
     slots = pool.entry_arrays(qsl, ids, flags)
     E, T = len(ids), int(qsl[-1])
     meta = BatchMeta(E, T, tile_tokens=128, device=device)
-    meta.set_slot_split(pool.slot_split)
-    meta.build_arrays(qsl, slots, flags)  # entries now resident in HBM
+    meta.build_arrays(qsl, slots, flags, slot_split=pool.slot_split)  # entries now resident in HBM
     dims = shape.site_dims()
     g = torch.Generator(device=device)
     g.manual_seed(1234 + rank)
@@ -275,7 +483,7 @@ def build_step(args, rank, world, device, n_prefill, n_decode, seed=SEED):
     sel_prefill = int(lens.sum())
     distinct = len({ids[i] for i in range(len(ids)) if not (flags[i] & 1)})
     return dict(shape=shape, pool=pool, meta=meta, plan=plan, acts=acts, qsl=qsl, ids=ids, flags=flags, slots=slots,
-                lens=lens, T=T, E=E, sel=sel_prefill, distinct=distinct, owned=owned)
+                lens=lens, T=T, E=E, sel=sel_prefill, distinct=distinct, owned=owned, rank=lora_rank)
 
 
 def time_steps(ctx, args, world, device, timing_tag=None):
@@ -306,10 +514,25 @@ def time_steps(ctx, args, world, device, timing_tag=None):
     return ms, kernel
 
 
+def parity_lora_plan(ctx, run_once, seed: int = 0) -> dict:
+    """One more run of the timed plan (every layer adds into the same y):
+    sampled rows of every site == y0 + sum of 32 layers' deltas (oracle)."""
+    import torch
+
+    snap = {g: [y.clone() for y in ys] for g, (x, ys) in ctx["acts"].items()}
+    run_once()
+    torch.cuda.synchronize()
+    out = check_lora_accumulated(ctx["pool"], ctx["meta"], ctx["qsl"], ctx["slots"], ctx["acts"], snap,
+                                 range(N_LAYERS), seed=seed, n_updates=N_LAYERS)
+    del snap
+    return out
+
+
 def run_e2e(ctx, args, world, device):
     """Host-buffer path: per step H2D of the entries + every layer's site
     activations from pinned memory, the kernels, D2H of every updated output.
-    Copies run on their own streams, double-buffered against compute."""
+    Copies run on their own streams, double-buffered against compute.  The
+    last layer's host outputs are checked against the oracle afterwards."""
     import torch
 
     from paper_2605_14217_b200 import shapes
@@ -340,7 +563,7 @@ def run_e2e(ctx, args, world, device):
     qsl, slots, flags = ctx["qsl"], ctx["slots"], ctx["flags"]
 
     def one_step():
-        meta.build_arrays(qsl, slots, flags, stream=comp)  # entries H2D + K1
+        meta.build_arrays(qsl, slots, flags, stream=comp, slot_split=pool.slot_split)  # entries H2D + K1
         for layer in range(N_LAYERS):
             b = layer % 2
             with torch.cuda.stream(up):
@@ -371,7 +594,7 @@ def run_e2e(ctx, args, world, device):
         one_step()
     torch.cuda.synchronize()
     barrier(world)
-    n = max(2, min(args.steps, 5))
+    n = max(3, min(args.steps, 10))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(comp)
     for _ in range(n):
@@ -380,7 +603,15 @@ def run_e2e(ctx, args, world, device):
     torch.cuda.synchronize()
     barrier(world)
     ms = e0.elapsed_time(e1) / n
-    return ms, N_LAYERS * h2d_bytes + meta.h2d_bytes, N_LAYERS * d2h_bytes, n
+    parity = None
+    if not args.no_parity:
+        # host_out[1] holds layer 31's outputs: host y + layer 31's delta of host x
+        last = N_LAYERS - 1
+        acts = {gp: (host_in[gp][0], host_out[last % 2][gp]) for gp in shapes.SITE_GROUPS}
+        snap = {gp: host_in[gp][1] for gp in shapes.SITE_GROUPS}
+        parity = check_lora_accumulated(pool, meta, qsl, slots, acts, snap, [last], seed=3)
+        parity["what"] = "host outputs of layer 31 (last step) vs host inputs + oracle delta"
+    return ms, N_LAYERS * h2d_bytes + meta.h2d_bytes, N_LAYERS * d2h_bytes, n, parity
 
 
 def punica_step(args, rank, world, device):
@@ -402,23 +633,60 @@ def punica_step(args, rank, world, device):
     e1.record(s)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
-    out = {"prefill_tokens": ctx["sel"], "ms_per_step": round(ms, 4),
-           "value": round(ctx["sel"] / (ms / 1e3), 1), "launch": "cuda graph"}
+    out = {"workload": "Punica-sized step: 32 prefill requests + 32 decode tokens (engine.py:101-112), cfg2 shapes",
+           "prefill_tokens": ctx["sel"], "ms_per_step": round(ms, 4),
+           "value": round(ctx["sel"] / (ms / 1e3), 1), "unit": UNIT, "launch": "cuda graph",
+           "rows_hint": ctx["plan"].rows_hint}
+    if not args.no_parity:
+        out["parity"] = parity_lora_plan(ctx, g.replay, seed=7)
     del ctx, g
     torch.cuda.empty_cache()
     return out
 
 
-def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, steps: int = 5,
-                world: int = 1, grank: int = 0) -> dict:
-    """Secondary line: a ReFT^P residual site x 32 layers (8B shapes) over one
-    batch of long prompts, one fused launch per layer (BASELINE configs 3/5).
-    With `world` GPUs each rank holds its shard of the 512 adapters (adapter
-    a lives on GPU a mod world) and serves prompts routed to them (weak
-    scaling, no collective on the data path)."""
+def lora_rank_config(args, device, rank_r: int = 16) -> dict:
+    """LoRA^P at rank 16 on one GPU through the standard apply path (8B shapes,
+    the cfg2 batch): where r makes the LoRA a contraction (~10.5 FLOP/B)."""
     import torch
 
-    from paper_2605_14217_b200 import AdapterKind, shapes
+    from paper_2605_14217_b200 import costs, shapes
+
+    ctx = build_step(args, 0, 1, device, args.requests, args.decodes, lora_rank=rank_r)
+    steps = max(3, min(args.steps, 10))
+    a2 = argparse.Namespace(**{**vars(args), "steps": steps, "warmup": 2})
+    ms, kernel = time_steps(ctx, a2, 1, device, timing_tag=1)
+    k_ms, k_n = kernel
+    dims = ctx["shape"].site_dims()
+    step_bytes = N_LAYERS * sum(costs.lora_group_bytes(dims, g, ctx["sel"], ctx["distinct"], rank_r)
+                                for g in shapes.SITE_GROUPS)
+    gu = costs.lora_group_bytes(dims, ("Wgate", "Wup"), ctx["sel"], ctx["distinct"], rank_r)
+    peak, _ = measured_peak_gbs()
+    out = {"workload": f"8B shapes, 512 LoRA^P r{rank_r} adapters, cfg2 batch ({ctx['sel']} prefill tokens), 1 GPU",
+           "prefill_tokens": ctx["sel"], "ms_per_step": round(ms / steps, 4),
+           "value": round(ctx["sel"] * steps / (ms / 1e3), 1), "unit": UNIT,
+           "step_frac_of_hbm_peak": round(step_bytes / (ms / steps / 1e3) / 1e9 / peak, 4),
+           "gate_up_frac_of_hbm_peak": round(gu / (k_ms / k_n / 1e3) / 1e9 / peak, 4),
+           "gate_up_avg_launch_us": round(k_ms / k_n * 1e3, 2)}
+    if not args.no_parity:
+        out["parity"] = parity_lora_plan(ctx, lambda: ctx["plan"].run(), seed=16)
+    del ctx
+    torch.cuda.empty_cache()
+    return out
+
+
+def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, steps: int = 5,
+                world: int = 1, grank: int = 0, owned=None, strong: dict | None = None) -> dict:
+    """A ReFT^P residual site x 32 layers (8B shapes) over one batch of long
+    prompts, one fused launch per layer (BASELINE configs 3/5).
+
+    Weak scaling (default): each rank holds its 512/world shard of the pool
+    (adapter a on GPU a mod world) and serves prompts routed to it, the
+    prompt set per rank fixed.  `owned` / `strong`: the caller routed one
+    global request stream (strong scaling) and passes this rank's adapters
+    (its shard plus hot replicas) and its requests."""
+    import torch
+
+    from paper_2605_14217_b200 import AdapterKind, costs, shapes
     from paper_2605_14217_b200.meta import BatchMeta
     from paper_2605_14217_b200.plan import StepPlan
     from paper_2605_14217_b200.pool import AdapterPool
@@ -426,8 +694,9 @@ def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, 
 
     d = shapes.LLAMA_8B.d_model
     kind = AdapterKind(kind_name)
-    owned = shard_adapters(N_ADAPTERS, grank, world)
-    ids = [int(owned[int(a) % len(owned)]) for a in ids]  # requests routed to this GPU's adapters
+    if owned is None:
+        owned = shard_adapters(N_ADAPTERS, grank, world)
+        ids = [int(owned[int(a) % len(owned)]) for a in ids]  # requests routed to this GPU's adapters
     pool = AdapterPool(N_LAYERS, d, reft_capacity=len(owned), reft_rank=rank, dtype=torch.bfloat16, device=device)
     pool.fill_synthetic_(0, kind, rank, seed=5 + grank, ids=owned)
     n_dec = 64
@@ -438,8 +707,7 @@ def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, 
     slots = pool.entry_arrays(qsl, eids, flags)
     T = int(qsl[-1])
     meta = BatchMeta(len(eids), T, tile_tokens=128, device=device)
-    meta.set_slot_split(pool.slot_split)
-    meta.build_arrays(qsl, slots, flags)
+    meta.build_arrays(qsl, slots, flags, slot_split=pool.slot_split)
     h = torch.randn(T, d, device=device, dtype=torch.float32).to(torch.bfloat16)
     plan = StepPlan(meta, pool, max_tokens=T)
     for layer in range(N_LAYERS):
@@ -456,22 +724,77 @@ def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, 
         plan.run(s)
     e1.record(s)
     torch.cuda.synchronize()
-    ms = all_max(e0.elapsed_time(e1) / steps, world)
+    my_ms = e0.elapsed_time(e1) / steps
+    ms = all_max(my_ms, world)
     k_ms, k_n = plan.collect_timing()
     sel = int(np.sum(lens))
-    sel_all = int(all_sum(sel, world))
+    per_rank_sel = all_gather_floats(sel, world)
+    sel_all = int(sum(per_rank_sel))
     distinct = len(set(int(a) for a in ids))
-    per_launch = sel * 2 * d * 2 + distinct * 2 * (2 * rank * d) + distinct * 4 * rank
+    per_launch = costs.reft_bytes(d, sel, distinct, rank)
     peak, _ = measured_peak_gbs()
     frac = per_launch / (k_ms / k_n / 1e3) / 1e9 / peak
     frac = all_sum(frac, world) / world
-    out = {"workload": label + (f" [{world} GPUs, adapter-sharded, weak scaling]" if world > 1 else ""),
-           "prefill_tokens": sel_all, "ms_per_step": round(ms, 3),
+    tag = ""
+    if strong:
+        tag = f" [{world} GPUs, one global stream routed to adapter owners + hot replicas, strong scaling]"
+    elif world > 1:
+        tag = f" [{world} GPUs, adapter-sharded, weak scaling]"
+    out = {"workload": label + tag, "prefill_tokens": sel_all, "ms_per_step": round(ms, 3),
            "value": round(sel_all / (ms / 1e3), 1), "unit": UNIT, "kernel_frac_of_hbm_peak": round(frac, 4),
-           "avg_launch_us": round(k_ms / k_n * 1e3, 2), "n_gpus": world}
+           "avg_launch_us": round(k_ms / k_n * 1e3, 2), "n_gpus": world,
+           "scaling": "strong" if strong else "weak"}
+    if world > 1:
+        mean = sel_all / world
+        out["per_rank_prefill_tokens"] = [int(v) for v in per_rank_sel]
+        out["token_imbalance_max_over_mean"] = round(max(per_rank_sel) / mean, 3) if mean else None
+    if strong:
+        out.update(strong)
+    if not args.no_parity:
+        mask = meta.mask_host()
+        sel_rows, _ = sample_rows(mask, qsl, 32, seed=5)
+        h0 = _np(h[torch.as_tensor(sel_rows, device=device)])
+        plan.run(s)
+        torch.cuda.synchronize()
+        par = {"plan_32_layers": check_reft_chain(pool, meta, qsl, slots, h, h0, sel_rows, range(N_LAYERS),
+                                                  "h <- bf16(h + delta_L(h)), L = 0..31"),
+               "single_launch": check_reft_single(pool, meta, qsl, slots, h, 0, seed=6)}
+        par["status"] = "pass" if all(v["status"] == "pass" for v in par.values()) else "FAIL"
+        if world > 1:
+            oks = all_sum(1.0 if par["status"] == "pass" else 0.0, world)
+            par["ranks_passed"] = int(oks)
+        out["parity"] = par
     del pool, meta, plan, h
     torch.cuda.empty_cache()
     return out
+
+
+def cfg5_strong(args, device, world: int, grank: int) -> dict:
+    """BASELINE config 5 as a multi-GPU serving problem: ONE global Zipf
+    request stream (workload.py:137-140) over 512 LoReFT^P r32 adapters,
+    prompts U[8k, 16k]; hot adapters (share > 0.5/world, e.g. adapter 0 with
+    ~15%) are replicated on every GPU (workload.hot_replicas) and every
+    request is routed to a GPU holding its adapter, least-loaded replica
+    first (workload.route_requests).  Total work is fixed as world grows."""
+    from paper_2605_14217_b200.workload import (AdapterMix, WorkloadConfig, assign_adapters, hot_replicas,
+                                                route_requests, shard_adapters)
+
+    n_req = 16
+    ids = [int(a) for a in assign_adapters(WorkloadConfig(n_req, N_ADAPTERS, AdapterMix.SKEWED, seed=11))]
+    lens = np.random.default_rng(12).integers(8192, 16385, size=n_req)
+    hot = hot_replicas(ids, world)
+    routes = route_requests(ids, world, hot, lens)
+    mine = routes[grank]
+    owned = sorted(set(shard_adapters(N_ADAPTERS, grank, world)) | {a for a, hs in hot.items() if grank in hs})
+    info = {"global_requests": n_req, "global_prefill_tokens": int(lens.sum()),
+            "hot_replicated_adapters": sorted(hot), "requests_per_rank": [len(r) for r in routes]}
+    if not mine:  # nothing routed here: still take part in the collectives with an idle step
+        mine_lens, mine_ids = [1], [owned[0]]
+    else:
+        mine_lens, mine_ids = [int(lens[i]) for i in mine], [ids[i] for i in mine]
+    return reft_config(args, device, "loreft", 32, mine_lens, mine_ids,
+                       "cfg5 strong: one Zipf stream of 16 prompts U[8k,16k] over 512 LoReFT^P r32 adapters x 32 layers",
+                       world=world, grank=grank, owned=owned, strong=info)
 
 
 def lora_reft_mix_config(args, device) -> dict:
@@ -487,16 +810,15 @@ def lora_reft_mix_config(args, device) -> dict:
     d = 4096
     pool = AdapterPool(1, d, lora_sites={"Wq": (d, d)}, lora_capacity=16, lora_rank=1, reft_capacity=16,
                        reft_rank=8, dtype=torch.bfloat16, device=device)
-    lora_ids = pool.fill_synthetic_(16, AdapterKind.LORA, 1, seed=1, ids=list(range(16, 32)))
-    reft_ids = pool.fill_synthetic_(16, AdapterKind.DIREFT, 8, seed=2, ids=list(range(16)))
+    pool.fill_synthetic_(16, AdapterKind.LORA, 1, seed=1, ids=list(range(16, 32)))
+    pool.fill_synthetic_(16, AdapterKind.DIREFT, 8, seed=2, ids=list(range(16)))
     lens = [1] * 32 + [128] * 32
     qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
     flags = np.array([1] * 32 + [0] * 32, dtype=np.int32)
     eids = [i % 32 for i in range(32)] + list(range(32))
     slots = pool.entry_arrays(qsl, eids, flags)
     meta = BatchMeta(64, int(qsl[-1]), device=device)
-    meta.set_slot_split(pool.slot_split)
-    meta.build_arrays(qsl, slots, flags)
+    meta.build_arrays(qsl, slots, flags, slot_split=pool.slot_split)
     T = int(qsl[-1])
     x = torch.randn(T, d, device=device).to(torch.bfloat16)
     y = torch.randn(T, d, device=device).to(torch.bfloat16)
@@ -516,11 +838,21 @@ def lora_reft_mix_config(args, device) -> dict:
     e1.record(s)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / n
+    out = {"workload": "cfg1: 1 layer d=4096, 16 DiReFT^P r8 + 16 LoRA^P r1, 32x128 prefill + 32 decode",
+           "prefill_tokens": 4096, "ms_per_step": round(ms, 4),
+           "value": round(4096 / (ms / 1e3), 1), "unit": "tokens/s per (layer, site pair)"}
+    if not args.no_parity:
+        y0 = y.clone()
+        meta.launch(s)
+        apply_lora_(y, x, meta, pool, 0, "Wq")
+        torch.cuda.synchronize()
+        lora = check_lora_accumulated(pool, meta, qsl, slots, {("Wq",): (x, [y])}, {("Wq",): [y0]}, [0], seed=1)
+        reft = check_reft_single(pool, meta, qsl, slots, h, 0, seed=2)
+        out["parity"] = {"status": "pass" if lora["status"] == reft["status"] == "pass" else "FAIL",
+                         "lora": lora, "reft": reft}
     del pool, meta
     torch.cuda.empty_cache()
-    return {"workload": "cfg1: 1 layer d=4096, 16 DiReFT^P r8 + 16 LoRA^P r1, 32x128 prefill + 32 decode",
-            "prefill_tokens": 4096, "ms_per_step": round(ms, 4),
-            "value": round(4096 / (ms / 1e3), 1), "unit": "tokens/s per (layer, site pair)"}
+    return out
 
 
 def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | None:
@@ -533,7 +865,7 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
     group and layer)."""
     import torch
 
-    from paper_2605_14217_b200 import AdapterKind, shapes
+    from paper_2605_14217_b200 import AdapterKind, costs, shapes
     from paper_2605_14217_b200.meta import BatchMeta
     from paper_2605_14217_b200.pool import AdapterPool
     from paper_2605_14217_b200.tp import SplitWorkspace, apply_lora_group_tp_
@@ -552,8 +884,7 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
     slots = pool.entry_arrays(qsl, ids, flags)
     T = int(qsl[-1])
     meta = BatchMeta(len(ids), T, tile_tokens=128, device=device)
-    meta.set_slot_split(pool.slot_split)
-    meta.build_arrays(qsl, slots, flags)
+    meta.build_arrays(qsl, slots, flags, slot_split=pool.slot_split)
     ws = SplitWorkspace(meta, pool)
     g = torch.Generator(device=device)
     g.manual_seed(77 + rank)
@@ -609,15 +940,11 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
     ms = all_max(e0.elapsed_time(e1) / steps, world)
     sel = int(lens.sum())
     distinct = len({ids[i] for i in range(len(ids)) if not (flags[i] & 1)})
-    # algorithmic bytes per rank per step (sharded): x slice read,
-    # y slice read + written, each distinct adapter's A / B shard once, P
-    # written by the shrink and read by the expand (f32)
     per_layer = 0
     for group in shapes.SITE_GROUPS:
         m_loc = pool.lora_shard[group[0]].m_loc
         n_locs = [pool.lora_shard[t].n_loc for t in group]
-        per_layer += sel * 2 * (m_loc + 2 * sum(n_locs)) + distinct * 2 * r * sum(m_loc + n for n in n_locs)
-        per_layer += 2 * sel * 4 * r * len(group)
+        per_layer += costs.split_group_bytes(m_loc, n_locs, sel, distinct, r)
     step_bytes = shape.n_layers * per_layer
     peak, _ = measured_peak_gbs()
     frac = step_bytes / (ms / 1e3) / 1e9 / peak
@@ -629,6 +956,31 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
            "per_rank_frac_of_hbm_peak": round(frac, 4), "per_rank_algorithmic_bytes": int(step_bytes),
            "allreduce_bytes_per_rank_per_step": int(allreduce_bytes) if real else 0,
            "pool_gb_per_rank": round(pool.nbytes / 1e9, 2), "launch": launch}
+    if not args.no_parity and not real:
+        # one more replay: set 0 takes the even layers' deltas (rank 0's partial
+        # shrink over its m-slice, its n-slice of B; no all-reduce on 1 GPU)
+        import torch as _t
+
+        acts0 = sets[0]
+        snap = {gp: [y.clone() for y in ys] for gp, (x, ys) in acts0.items()}
+        replay()
+        _t.cuda.synchronize()
+        mask = meta.mask_host()
+        sel_rows, _ = sample_rows(mask, qsl, 24, seed=4)
+        row_slots = np.asarray(slots)[_row_entries(qsl, sel_rows)]
+        errs = []
+        idx = _t.as_tensor(sel_rows, device=device)
+        for gp, (x, ys) in acts0.items():
+            xr = _np(x[idx])
+            for sname, y, y0 in zip(gp, ys, snap[gp]):
+                d_ref = lora_rows_delta(pool, range(0, shape.n_layers, 2), sname, row_slots, xr, shard=True)
+                base, outr = _np(y0[idx]), _np(y[idx])
+                errs.append(_rel(outr, base + d_ref))
+        out["parity"] = _verdict(errs, len(sel_rows), 2e-2, {"what": "rank 0 shard: y_slice += sum over its 40 "
+                                                             "layers of s (x_mslice A_shard^T) B_shard^T"})
+    elif real:
+        out["parity"] = {"status": "not checked on the multi-rank run (the kernels' TP=8 parity is "
+                                   "tests/test_gpu_tp.py at 70B shard widths)"}
     del pool, meta, ws, sets, graph
     torch.cuda.empty_cache()
     return out
@@ -654,12 +1006,12 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
     from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig
 
     shape = shapes.LLAMA_8B
-    slots = 32
-    pool = AdapterPool(N_LAYERS, shape.d_model, lora_sites=shape.site_dims(), lora_capacity=slots, lora_rank=RANK,
+    slots_n = 32
+    pool = AdapterPool(N_LAYERS, shape.d_model, lora_sites=shape.site_dims(), lora_capacity=slots_n, lora_rank=RANK,
                        dtype=torch.bfloat16, device=device)
     snaps = {}
-    for first in range(0, N_ADAPTERS, slots):  # pinned host slot images of all 512 adapters
-        ids = list(range(first, min(N_ADAPTERS, first + slots)))
+    for first in range(0, N_ADAPTERS, slots_n):  # pinned host slot images of all 512 adapters
+        ids = list(range(first, min(N_ADAPTERS, first + slots_n)))
         pool.fill_synthetic_(0, AdapterKind.LORA, RANK, seed=100 + first, sigma=0.01, ids=ids)
         for a in ids:
             snaps[a] = pool.export_slot(a)
@@ -667,21 +1019,26 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
         for a in ids:
             pool.unregister(a, zero=False)
     paged = PagedAdapterPool(pool, {}, snapshots=snaps)
-    cfg = ServeConfig(max_batch=32, max_gpu_adapters=slots, step_token_budget=2048)
+    cfg = ServeConfig(max_batch=32, max_gpu_adapters=slots_n, step_token_budget=2048)
     meta = BatchMeta(cfg.max_batch, cfg.step_token_budget, tile_tokens=128, device=device)
     dims = shape.site_dims()
     g = torch.Generator(device=device)
     g.manual_seed(5)
     T = cfg.step_token_budget
-    plan = StepPlan(meta, pool, max_tokens=T)
+    wl = generate_workload(WorkloadConfig(n_requests, N_ADAPTERS, AdapterMix.UNIFORM, seed=0, l_max=l_max))
+    # the K2 launch shape baked into the captured graph: the mean selected
+    # rows of this schedule's adapter-carrying steps (host-known up front)
+    counts = [st.prefill_tokens for st in Scheduler(wl, cfg, PositionSchedule.PREFILL_ONLY) if st.prefill_tokens]
+    hint = int(np.mean(counts)) if counts else T
+    plan = StepPlan(meta, pool, max_tokens=T, rows_hint=hint)
+    bufs = {}
     for layer in range(N_LAYERS):
         for group in shapes.SITE_GROUPS:
             x = torch.randn(T, dims[group[0]][1], generator=g, device=device).to(torch.bfloat16)
             ys = [torch.randn(T, dims[t][0], generator=g, device=device).to(torch.bfloat16) for t in group]
             plan.add_lora_group(ys, x, layer, group)
-    wl = generate_workload(WorkloadConfig(n_requests, N_ADAPTERS, AdapterMix.UNIFORM, seed=0, l_max=l_max))
+            bufs[(layer, group)] = (x, ys)
     s = torch.cuda.current_stream(device)
-    from paper_2605_14217_b200 import _lib
 
     # the 128 site launches of a step as one CUDA graph (a serving engine's
     # decode-graph practice); metadata is rebuilt eagerly before each replay
@@ -690,6 +1047,7 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
         graph = plan.capture(run_meta=False)
     except Exception:  # capture unsupported here: eager launches through the native plan
         graph = None
+    last = {}
 
     def run(limit=None):
         steps = toks = pre = 0
@@ -698,13 +1056,15 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
             # all-unselected steps skip the adapter path, decided on the host
             # (forward_chunk's skip_adapters, model.py:475): decode-only steps
             # of prefill-only adapters launch nothing
-            if any(a is not None and not d for a, d in zip(step.adapter_ids, step.decode_flags)):
-                flags = (step.decode_flags * _lib.ENTRY_DECODE).astype(np.int32)
-                meta.build_arrays(step.qsl, pool.entry_arrays(step.qsl, step.adapter_ids, flags), flags, stream=s)
+            if step.workset:
+                flags = step.entry_flags()
+                slots = pool.entry_arrays(step.qsl, step.adapter_ids, flags)
+                meta.build_arrays(step.qsl, slots, flags, stream=s, slot_split=pool.slot_split)
                 if graph is not None:
                     graph.replay()
                 else:
                     plan.run(s, run_meta=False)
+                last.update(qsl=step.qsl, slots=slots, flags=flags)
             steps += 1
             toks += step.tokens
             pre += step.prefill_tokens
@@ -726,43 +1086,101 @@ def serving_replay(args, device, n_requests: int = 128, l_max: int = 256) -> dic
            "steps": steps, "tokens": toks, "prefill_tokens": pre, "ms": round(ms, 2),
            "value": round(toks / (ms / 1e3), 1), "unit": "tokens/s (prompt + generated)",
            "page_ins": paged.page_ins - p0, "paged_gb": round((paged.paged_bytes - b0) / 1e9, 2),
-           "launch": "cuda graph per step (site launches), eager paging + K1" if graph is not None else "eager"}
-    del graph, plan, pool, paged, snaps
+           "launch": "cuda graph per step (site launches), eager paging + K1" if graph is not None else "eager",
+           "rows_hint": hint}
+    if not args.no_parity and last:
+        # the last adapter-carrying step again (its adapters are still resident):
+        # layers 0 and 31 of every group vs the oracle
+        meta.build_arrays(last["qsl"], last["slots"], last["flags"], stream=s, slot_split=pool.slot_split)
+        chk = {(L, gp): bufs[(L, gp)] for L in (0, N_LAYERS - 1) for gp in shapes.SITE_GROUPS}
+        snap = {k: [y.clone() for y in v[1]] for k, v in chk.items()}
+        graph.replay() if graph is not None else plan.run(s, run_meta=False)
+        torch.cuda.synchronize()
+        res = [check_lora_accumulated(pool, meta, last["qsl"], last["slots"], {k[1]: v}, {k[1]: snap[k]}, [k[0]],
+                                      k=24, seed=9) for k, v in chk.items()]
+        worst = max(r["max_rel_err"] for r in res)
+        out["parity"] = {"status": "pass" if all(r["status"] == "pass" for r in res) else "FAIL",
+                         "rows_checked": res[0]["rows_checked"], "max_rel_err": worst, "tol": 2e-2,
+                         "what": "last scheduled step replayed: layers 0 and 31, every site, vs the oracle"}
+    del graph, plan, pool, paged, snaps, bufs
     torch.cuda.empty_cache()
     return out
 
 
-def secondary_configs(args, device, world: int = 1, rank: int = 0) -> list:
-    from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig, assign_adapters
-
-    out = [lora_reft_mix_config(args, device)] if world == 1 else []
-    rng = np.random.default_rng(3)
-    ids3 = rng.integers(0, N_ADAPTERS, size=32)
-    out.append(reft_config(args, device, "direft", 16, [2048] * 32, ids3,
-                           "cfg3: 8B shapes, DiReFT^P r16 x 32 layers, 512 adapters, 32 x 2048-token prompts + 64 decode "
-                           "per GPU", world=world, grank=rank))
-    ids5 = assign_adapters(WorkloadConfig(8, N_ADAPTERS, AdapterMix.SKEWED, seed=5))
-    lens5 = rng.integers(8192, 16385, size=8)
-    out.append(reft_config(args, device, "loreft", 32, lens5, ids5,
-                           "cfg5: Zipf over 512 adapters, 8 prompts U[8k,16k] per GPU, LoReFT^P r32 x 32 layers",
-                           world=world, grank=rank))
-    if world == 1:
-        out.append(serving_replay(args, device))
-    return out
-
-
 def cpu_baseline(ctx, seconds: float) -> dict:
-    """The reference CPU path (float64 numpy oracle) on one host core, on a
-    bounded sample of the same workload: the first 8 prefill requests (plus
-    every decode entry for the mask) through 7 sites of a rotating layer."""
+    """The reference's CPU path (prefillsim from oracle/_ref, else the oracle
+    port) on one host core, on a bounded sample of the same workload: the
+    first 8 prefill requests (plus 8 decode entries) through all 32 layers."""
     from threadpoolctl import threadpool_limits
 
     from oracle import cpu_reference as CR
 
     with threadpool_limits(1):
         res = CR.time_sample(ctx["qsl"], ctx["ids"], ctx["flags"], n_requests=8, seconds=seconds, seed=SEED)
-    return {"value": round(res["tokens_per_s"], 3), "unit": UNIT, "cores": 1, "kind": "port",
+    return {"value": round(res["tokens_per_s"], 3), "unit": UNIT, "cores": 1, "kind": res["kind"],
             "sample": res["sample"]}
+
+
+def cfg2_config(args, world: int, sel: int, T: int, E: int, distinct: int, tokens_all: int) -> dict:
+    return {
+        "workload": "cfg2 Uniform Punica saturating step: Llama-3.1-8B shapes, 32 layers x 7 LoRA^P sites "
+                    "(4 fused groups), 512 LoRA^P r=1 adapters sharded by id, per GPU "
+                    f"{args.requests} prefill requests (Punica lengths) + {args.decodes} decode tokens",
+        "model": "Llama-3.1-8B projection shapes (GQA k/v 1024), random init",
+        "adapters": N_ADAPTERS,
+        "rank": RANK,
+        "prefill_tokens_per_gpu": sel,
+        "tokens_per_gpu": T,
+        "entries_per_gpu": E,
+        "distinct_adapters_per_gpu": distinct,
+        "global_batch": int(tokens_all),
+        "seq_len": "ragged (Punica lognormal prompts)",
+        "parallelism": f"adapter-sharded replicas x{world} (requests routed to adapter owner, no collective)",
+        "l2_policy": "inputs larger than L2: ~0.9 GB of per-layer activations stream between reuses (L2 126 MB)",
+    }
+
+
+SECONDARY = ("cfg1", "cfg3", "cfg5", "cfg5s", "lora16", "serving", "cfg4")
+
+
+def secondary_lines(args, device, world: int, rank: int, only: set[str]) -> list:
+    """Every BASELINE config that is not the headline, each with its parity.
+    A failure in one line is recorded in that line, never loses the others."""
+    import torch
+
+    from paper_2605_14217_b200.workload import AdapterMix, WorkloadConfig, assign_adapters
+
+    want = (lambda k: k in only) if only else (lambda k: True)
+    rng = np.random.default_rng(3)
+    ids3 = rng.integers(0, N_ADAPTERS, size=32)
+    ids5 = assign_adapters(WorkloadConfig(8, N_ADAPTERS, AdapterMix.SKEWED, seed=5))
+    lens5 = rng.integers(8192, 16385, size=8)
+    jobs = [
+        ("cfg1", world == 1, lambda: lora_reft_mix_config(args, device)),
+        ("cfg3", True, lambda: reft_config(args, device, "direft", 16, [2048] * 32, ids3,
+                                           "cfg3: 8B shapes, DiReFT^P r16 x 32 layers, 512 adapters, 32 x 2048-token "
+                                           "prompts + 64 decode per GPU", world=world, grank=rank)),
+        ("cfg5", True, lambda: reft_config(args, device, "loreft", 32, lens5, ids5,
+                                           "cfg5: Zipf over 512 adapters, 8 prompts U[8k,16k] per GPU, LoReFT^P r32 "
+                                           "x 32 layers", world=world, grank=rank)),
+        ("cfg5s", True, lambda: cfg5_strong(args, device, world, rank)),
+        ("lora16", world == 1, lambda: lora_rank_config(args, device, 16)),
+        ("serving", world == 1, lambda: serving_replay(args, device)),
+        ("cfg4", world in (1, 8), lambda: tp_config(args, device, world, rank)),
+    ]
+    out = []
+    for key, ok, fn in jobs:
+        if not (ok and want(key)):
+            continue
+        try:
+            line = fn()
+        except Exception as exc:  # never lose the headline line to a secondary config
+            line = {"workload": key, "error": f"{type(exc).__name__}: {exc}"[:300]}
+            torch.cuda.empty_cache()
+        if line is not None:
+            line["key"] = key
+            out.append(line)
+    return out
 
 
 def run_ours(args):
@@ -771,6 +1189,17 @@ def run_ours(args):
     world, rank, local = dist_setup(args)
     dist_init(world, local)
     device = torch.device("cuda", local)
+    only = {k for k in args.only.split(",") if k}
+    if only:
+        others = []
+        if "punica" in only and world == 1:
+            others.append(punica_step(args, rank, world, device))
+        others += secondary_lines(args, device, world, rank, only)
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "only": sorted(only), "n_gpus": world, "other_configs": others}))
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
     ctx = build_step(args, rank, world, device, args.requests, args.decodes)
     clocks = ClockSampler(local)
     clocks.start()
@@ -792,32 +1221,31 @@ def run_ours(args):
     step_bytes = N_LAYERS * sum(group_bytes(shape, gp, ctx["sel"], ctx["distinct"]) for gp in shapes.SITE_GROUPS)
     step_s = ms_total / args.steps / 1e3
     gpu_launches = ctx["plan"].launches_per_run * args.steps
+    parity = None
+    if not args.no_parity:
+        parity = parity_lora_plan(ctx, lambda: ctx["plan"].run(), seed=rank)
+        if world > 1:
+            parity["ranks_passed"] = int(all_sum(1.0 if parity["status"] == "pass" else 0.0, world))
 
     e2e = None
     if not args.no_e2e:
-        e_ms, bi, bo, n = run_e2e(ctx, args, world, device)
+        e_ms, bi, bo, n, e_par = run_e2e(ctx, args, world, device)
         e_ms = all_max(e_ms, world)
         e2e = {"value": round(tokens_all / (e_ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(bi),
                "d2h_bytes_per_step": int(bo), "ms_per_step": round(e_ms, 3), "steps": n,
-               "path": "pinned host x/y of every layer -> device -> fused kernels -> host, copy streams overlapped"}
+               "path": "pinned host x/y of every layer -> device -> fused kernels -> host, copy streams overlapped",
+               "parity": e_par}
     punica = None
     if not args.no_punica_step and world == 1:
         punica = punica_step(args, rank, world, device)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(ctx, args.cpu_seconds)
     others = None
     if not args.no_secondary:
         del ctx["plan"], ctx["acts"]
         torch.cuda.empty_cache()
-        others = secondary_configs(args, device, world, rank)
-        try:
-            cfg4 = tp_config(args, device, world, rank)
-        except Exception as exc:  # never lose the headline line to the secondary config
-            cfg4 = {"workload": "cfg4 (70B, TP=8)", "error": f"{type(exc).__name__}: {exc}"[:300]}
-            torch.cuda.empty_cache()
-        if cfg4 is not None:
-            others.append(cfg4)
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(ctx, args.cpu_seconds)
+        others = secondary_lines(args, device, world, rank, set())
     if rank == 0:
         line = {
             "metric": METRIC,
@@ -832,22 +1260,8 @@ def run_ours(args):
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (random adapters N(0,0.01^2), random bf16 activations, Punica prompt lengths)",
-            "config": {
-                "workload": "cfg2 Uniform Punica saturating step: Llama-3.1-8B shapes, 32 layers x 7 LoRA^P sites "
-                            "(4 fused groups), 512 LoRA^P r=1 adapters sharded by id, per GPU "
-                            f"{args.requests} prefill requests (Punica lengths) + {args.decodes} decode tokens",
-                "model": "Llama-3.1-8B projection shapes (GQA k/v 1024), random init",
-                "adapters": N_ADAPTERS,
-                "rank": RANK,
-                "prefill_tokens_per_gpu": ctx["sel"],
-                "tokens_per_gpu": ctx["T"],
-                "entries_per_gpu": ctx["E"],
-                "distinct_adapters_per_gpu": ctx["distinct"],
-                "global_batch": int(tokens_all),
-                "seq_len": "ragged (Punica lognormal prompts)",
-                "parallelism": f"adapter-sharded replicas x{world} (requests routed to adapter owner, no collective)",
-                "l2_policy": "inputs larger than L2: ~0.9 GB of per-layer activations stream between reuses (L2 126 MB)",
-            },
+            "config": cfg2_config(args, world, ctx["sel"], ctx["T"], ctx["E"], ctx["distinct"], tokens_all),
+            "parity": parity,
             "roofline": {
                 "bound": "hbm",
                 "kernel": "lora_team_kernel<bf16,R=1,NS=2,U=4,TEAM=1> (K2, gate/up fused group)",
@@ -882,46 +1296,95 @@ def run_ours(args):
 
 
 def run_reference(args):
+    """The reference's own CPU implementation of this path (prefillsim,
+    unmodified, from oracle/_ref; else the pinned oracle port) on every host
+    core, over the SAME cfg2 batch as the GPU arm: each step is the whole
+    batch through all 32 layers x 7 LoRA^P sites."""
     world, rank, local = dist_setup(args)
     if rank != 0:
         return  # rank 0 alone runs the CPU reference
     from oracle import cpu_reference as CR
 
     qsl, ids, flags, lens, owned = step_entries(0, 1, args.requests, args.decodes)
-    cores = len(os.sched_getaffinity(0))
-    res = CR.time_parallel(qsl, ids, flags, cores=cores, per_worker_requests=args.ref_requests, steps=args.steps,
-                           warmup=args.warmup, seed=SEED)
+    cores = args.ref_cores or len(os.sched_getaffinity(0))
+    steps, warmup = max(1, args.steps), max(1, min(args.warmup, 2))
+    res = CR.time_parallel(qsl, ids, flags, cores=cores, steps=steps, warmup=warmup, seed=SEED)
     value = res["tokens_per_s"]
+    distinct = len({ids[i] for i in range(len(ids)) if not (flags[i] & 1)})
+    T, E, sel = int(qsl[-1]), len(ids), int(lens.sum())
     line = {
         "metric": METRIC,
         "value": round(value, 3),
         "unit": UNIT,
         "n_gpus": args.gpus,
-        "steps": args.steps,
-        "warmup": args.warmup,
+        "steps": steps,
+        "warmup": warmup,
         "ms_per_step": round(res["ms_per_step"], 3),
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": None,
         "dtype": "f64",
-        "data": "synthetic, same workload generator as the GPU arm",
+        "data": "synthetic (random adapters N(0,0.01^2), random activations, Punica prompt lengths), same batch as "
+                "the GPU arm",
         "impl": "reference",
-        "config": {
-            "workload": "cfg2 Uniform Punica: Llama-3.1-8B shapes, 7 LoRA^P sites per layer, 512 LoRA^P r=1 adapters",
-            "model": "Llama-3.1-8B projection shapes, random init",
-            "adapters": N_ADAPTERS,
-            "rank": RANK,
-        },
-        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": "port",
+        "config": cfg2_config(args, 1, sel, T, E, distinct, sel),
+        "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": cores, "kind": res["kind"],
                          "sample": res["sample"]},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
+# ---------------------------------------------------------------- launcher dry run (CPU, gloo)
+
+
+def run_dry(args):
+    """The multi-rank plumbing without kernels: rank/world from torchrun, a
+    gloo process group, each rank's adapter shard and routed cfg2 batch, the
+    cfg5 strong-scaling routing with hot replicas, and the max/sum
+    collectives; rank 0 prints the line.  tests/test_bench_launcher.py runs
+    `bench.py --gpus 2 --dry-run` through the same self-launch code."""
+    from paper_2605_14217_b200.workload import (AdapterMix, WorkloadConfig, assign_adapters, hot_replicas,
+                                                route_requests)
+
+    world, rank, local = dist_setup(args)
+    dist_init(world, local, backend="gloo")
+    qsl, ids, flags, lens, owned = step_entries(rank, world, args.requests, args.decodes)
+    assert all(a in set(owned) for a in ids), "a request routed to a GPU that does not own its adapter"
+    sel = int(lens.sum())
+    tok = all_gather_floats(sel, world)
+    t0 = time.perf_counter()
+    barrier(world)
+    ms = all_max((time.perf_counter() - t0) * 1e3, world)
+    n_req = 16
+    zids = [int(a) for a in assign_adapters(WorkloadConfig(n_req, N_ADAPTERS, AdapterMix.SKEWED, seed=11))]
+    zl = np.random.default_rng(12).integers(8192, 16385, size=n_req)
+    hot = hot_replicas(zids, world)
+    routes = route_requests(zids, world, hot, zl)
+    mine = sum(int(zl[i]) for i in routes[rank])
+    zt = all_gather_floats(mine, world)
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "backend": "gloo",
+                          "per_rank_prefill_tokens": [int(v) for v in tok], "global_prefill_tokens": int(sum(tok)),
+                          "barrier_ms_max": round(ms, 3),
+                          "cfg5_strong": {"hot_replicated_adapters": sorted(hot),
+                                          "per_rank_prefill_tokens": [int(v) for v in zt],
+                                          "global_prefill_tokens": int(zl.sum())}}))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
-    if args.impl == "reference":
+    if args.impl == "reference" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        run_reference(args)  # rank 0's work only: no need to launch the other ranks
+        return
+    maybe_self_launch(args)
+    if args.dry_run:
+        run_dry(args)
+    elif args.impl == "reference":
         run_reference(args)
     else:
         run_ours(args)

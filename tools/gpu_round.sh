@@ -43,7 +43,7 @@ python tools/ncu_summary.py --rep $O/${TAG}_prof.ncu-rep --launches $O/${TAG}_la
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:reft_tc -s 3 -c 1 -o $O/${TAG}_reft_prof \
   python tools/reft_bench.py --case cfg3 --variant tc --iters 1 > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none -k regex:"shrink_tc|expand_tc" -s 8 -c 8 -o $O/${TAG}_split_prof \
-  python tools/tp_bench.py > /dev/null 2>&1
+  python bench.py --only cfg4 --no-parity --steps 1 > /dev/null 2>&1
 # full reports are large (the 64 MiB return limit): keep CSV exports of the secondary captures
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:reft_res -s 3 -c 1 -o $O/${TAG}_res_prof \
   python tools/reft_bench.py --case cfg3 --variant res --d 2048 --iters 1 > /dev/null 2>&1
