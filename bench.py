@@ -303,6 +303,13 @@ def _row_entries(qsl: np.ndarray, rows: np.ndarray) -> np.ndarray:
     return np.searchsorted(np.asarray(qsl), rows, side="right") - 1
 
 
+def class_mask(mask: np.ndarray, qsl, slots, pool, lora: bool) -> np.ndarray:
+    """Rows a LoRA (or ReFT) launch adds to: selected rows whose slot is of
+    that class (slots below pool.slot_split are LoRA adapters)."""
+    row_slot = np.asarray(slots)[_row_entries(qsl, np.arange(len(mask)))]
+    return mask & ((row_slot < pool.slot_split) if lora else (row_slot >= pool.slot_split))
+
+
 def sample_rows(mask: np.ndarray, qsl, k: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
     """(selected rows, unselected rows): k selected rows spread over the
     entries (first/last rows of the longest entries included) + up to 8
@@ -364,7 +371,7 @@ def check_lora_accumulated(pool, meta, qsl, slots, groups_acts, snapshot, layers
     {group: [y0 per site]} taken just before the run."""
     import torch
 
-    mask = meta.mask_host()
+    mask = class_mask(meta.mask_host(), qsl, slots, pool, lora=True)
     sel, uns = sample_rows(mask, qsl, k, seed)
     ent = _row_entries(qsl, sel)
     row_slots = np.asarray(slots)[ent]
@@ -417,7 +424,7 @@ def check_reft_single(pool, meta, qsl, slots, h, layer: int, k=48, seed=0) -> di
     from oracle import preft_oracle as O
     from paper_2605_14217_b200.ops import apply_reft_
 
-    mask = meta.mask_host()
+    mask = class_mask(meta.mask_host(), qsl, slots, pool, lora=False)
     sel, uns = sample_rows(mask, qsl, k, seed)
     hc = h.clone()
     apply_reft_(hc, meta, pool, layer)
@@ -519,6 +526,13 @@ def parity_lora_plan(ctx, run_once, seed: int = 0) -> dict:
     sampled rows of every site == y0 + sum of 32 layers' deltas (oracle)."""
     import torch
 
+    # the timed steps added the same deltas into y again and again (|y| grows
+    # until bf16 cannot resolve one delta): restart from fresh N(0, 1) outputs
+    gen = torch.Generator(device=ctx["pool"].device)
+    gen.manual_seed(4242 + seed)
+    for x, ys in ctx["acts"].values():
+        for y in ys:
+            y.copy_(torch.randn(y.shape, generator=gen, device=y.device))
     snap = {g: [y.clone() for y in ys] for g, (x, ys) in ctx["acts"].items()}
     run_once()
     torch.cuda.synchronize()
@@ -751,7 +765,8 @@ def reft_config(args, device, kind_name: str, rank: int, lens, ids, label: str, 
     if strong:
         out.update(strong)
     if not args.no_parity:
-        mask = meta.mask_host()
+        h.copy_(torch.randn(h.shape, device=device))  # fresh activations (the timed steps edited h 32 x steps times)
+        mask = class_mask(meta.mask_host(), qsl, slots, pool, lora=False)
         sel_rows, _ = sample_rows(mask, qsl, 32, seed=5)
         h0 = _np(h[torch.as_tensor(sel_rows, device=device)])
         plan.run(s)
@@ -842,6 +857,8 @@ def lora_reft_mix_config(args, device) -> dict:
            "prefill_tokens": 4096, "ms_per_step": round(ms, 4),
            "value": round(4096 / (ms / 1e3), 1), "unit": "tokens/s per (layer, site pair)"}
     if not args.no_parity:
+        y.copy_(torch.randn(y.shape, device=device))  # fresh: the timed loop added the same delta 53 times
+        h.copy_(torch.randn(h.shape, device=device))
         y0 = y.clone()
         meta.launch(s)
         apply_lora_(y, x, meta, pool, 0, "Wq")
@@ -962,20 +979,30 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
         import torch as _t
 
         acts0 = sets[0]
+        for x, ys in acts0.values():
+            for y in ys:
+                y.copy_(_t.randn(y.shape, device=device))
         snap = {gp: [y.clone() for y in ys] for gp, (x, ys) in acts0.items()}
         replay()
         _t.cuda.synchronize()
-        mask = meta.mask_host()
+        mask = class_mask(meta.mask_host(), qsl, slots, pool, lora=True)
         sel_rows, _ = sample_rows(mask, qsl, 24, seed=4)
         row_slots = np.asarray(slots)[_row_entries(qsl, sel_rows)]
         errs = []
         idx = _t.as_tensor(sel_rows, device=device)
         for gp, (x, ys) in acts0.items():
-            xr = _np(x[idx])
+            sh0 = pool.lora_shard[gp[0]]
+            xr = _np(x[idx])[:, sh0.x_offset: sh0.x_offset + sh0.m_loc]  # the m-slice this rank's A covers
             for sname, y, y0 in zip(gp, ys, snap[gp]):
+                sh = pool.lora_shard[sname]
+                cols = slice(sh.y_offset, sh.y_offset + sh.n_loc)  # the n-slice this rank adds into
                 d_ref = lora_rows_delta(pool, range(0, shape.n_layers, 2), sname, row_slots, xr, shard=True)
                 base, outr = _np(y0[idx]), _np(y[idx])
-                errs.append(_rel(outr, base + d_ref))
+                errs.append(_rel(outr[:, cols], base[:, cols] + d_ref))
+                rest = np.ones(outr.shape[1], bool)
+                rest[cols] = False
+                if rest.any() and not np.array_equal(outr[:, rest], base[:, rest]):
+                    errs.append(float("inf"))  # columns outside the rank's slice must stay untouched
         out["parity"] = _verdict(errs, len(sel_rows), 2e-2, {"what": "rank 0 shard: y_slice += sum over its 40 "
                                                              "layers of s (x_mslice A_shard^T) B_shard^T"})
     elif real:

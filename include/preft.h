@@ -42,7 +42,7 @@
 extern "C" {
 #endif
 
-#define PREFT_ABI_VERSION 1
+#define PREFT_ABI_VERSION 2
 
 /* status codes (errors.py:8-37) */
 #define PREFT_OK 0
@@ -142,6 +142,9 @@ typedef struct preft_meta {
     int32_t* units;
     int32_t chunk_cap;   /* >= E_cap + T_cap / PREFT_CHUNK_ROWS + 1 (bounds chunks and units) */
     int32_t reserved;
+    float* lora_part;    /* NULL, or a [T_cap][nsites * r_max] f32 workspace for the rank-r
+                            intermediate of tensor-core LoRA launches (bf16, r_max 16/32) */
+    int64_t lora_part_floats; /* capacity of lora_part in floats */
 } preft_meta_t;
 
 #define PREFT_MAX_ENTRIES 4096
@@ -182,6 +185,12 @@ typedef struct preft_lora_site {
  * Unselected rows of y are never read or written.
  *   x: [T][ldx] (dtype), m = input width; nsites in 1..3; r_max in
  *   {1,2,4,8,16,32,64} with nsites * r_max <= 64.
+ * bf16 with r_max 16/32 (where the delta is a real contraction, ~10 FLOP/B
+ * at r = 16), m % 256 == 0, every n % 128 == 0, every site's Bt_tc given and
+ * meta->lora_part large enough runs on tcgen05: the split shrink into
+ * meta->lora_part (L2-resident, T x nsites x r f32) then the split expand
+ * (the same kernels as preft_lora_shrink / preft_lora_expand, no collective).
+ * Everything else runs the SIMT kernels (team / warp per row).
  */
 int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32_t m,
                      const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
@@ -280,6 +289,9 @@ int preft_plan_set_slot_split(preft_plan_t* plan, int32_t slot_split);
  * later run; a plan created before its meta's first build would otherwise
  * keep the hint 0 (one-warp teams).  Never affects results. */
 int preft_plan_set_rows_hint(preft_plan_t* plan, int32_t rows_hint);
+/* re-copy the meta descriptor (e.g. after its lora_part workspace was
+ * attached); the plan keeps its own slot_split and rows_hint */
+int preft_plan_refresh_meta(preft_plan_t* plan, const preft_meta_t* meta);
 int preft_plan_add_lora(preft_plan_t* plan, const void* x, int64_t ldx, int32_t m,
                         const preft_lora_site_t* sites, int32_t nsites, int32_t r_max,
                         int32_t dtype, int32_t tag);

@@ -45,7 +45,7 @@ UNIT_CHUNKS = 4
 SLOT_SPLIT_ALL_LORA = 2**31 - 1  # every slot is a LoRA-class slot
 MAX_ENTRIES = 4096
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class PreftMeta(ctypes.Structure):
@@ -67,6 +67,8 @@ class PreftMeta(ctypes.Structure):
         ("units", ctypes.c_void_p),
         ("chunk_cap", ctypes.c_int32),
         ("reserved", ctypes.c_int32),
+        ("lora_part", ctypes.c_void_p),
+        ("lora_part_floats", ctypes.c_int64),
     ]
 
 
@@ -175,6 +177,7 @@ SIGNATURES = {
     "preft_plan_destroy": (None, [ctypes.c_void_p]),
     "preft_plan_set_slot_split": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
     "preft_plan_set_rows_hint": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_int32]),
+    "preft_plan_refresh_meta": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(PreftMeta)]),
     "preft_plan_add_lora": (
         ctypes.c_int,
         [

@@ -206,6 +206,13 @@ void set_lora_variant(int v) { g_lora_variant = v; }
 
 int grid_for(const void* fn, int threads, int num_sms);
 bool pdl_enabled();
+bool lora_tc_route_ok(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
+                      int nsites, int r, int dtype);
+int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
+                const preft_lora_site_t* sites, int nsites, int r, int dtype, void* P, long long ldp,
+                cudaStream_t stream, int num_sms);
+int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long long rows, const preft_lora_site_t* sites,
+                int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
 
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
                int nsites, int r, int dtype, cudaStream_t stream, int num_sms) {
@@ -218,6 +225,18 @@ int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, co
         const preft_lora_site_t& st = sites[s];
         if (!st.A || !st.Bt || !st.scale || !st.y || st.n < 1 || st.ldy < st.n) return PREFT_ERR_SHAPE;
         vec = vec && (st.n % W == 0) && (st.ldy % W == 0) && aligned16(st.y) && aligned16(st.A) && aligned16(st.Bt);
+    }
+    // r >= 16 (bf16): ~10 FLOP/B at r = 16, beyond SIMT FP32 at the HBM
+    // roofline, so the delta goes through the tcgen05 split pair with the
+    // rank-r intermediate in the meta's workspace (T x nsites x r f32, stays
+    // in L2 between the two launches).  Both kernels only touch rows of the
+    // K1 units, so the TMA bound T_cap never exposes rows beyond the batch.
+    if (lora_variant() != 0 && lora_tc_route_ok(meta, x, ldx, m, sites, nsites, r, dtype)) {
+        const long long ldp = static_cast<long long>(nsites) * r;
+        int rc = lora_shrink(meta, x, meta->T_cap, ldx, m, sites, nsites, r, dtype, meta->lora_part, ldp, stream,
+                             num_sms);
+        if (rc) return rc;
+        return lora_expand(meta, meta->lora_part, ldp, meta->T_cap, sites, nsites, r, dtype, stream, num_sms);
     }
     if ((!vec || dtype == PREFT_DTYPE_F64) && nsites > 1) {  // one launch per site
         for (int s = 0; s < nsites; ++s) {

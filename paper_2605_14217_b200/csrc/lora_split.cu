@@ -771,19 +771,6 @@ SplitFn pick_split(bool vec, int nsites, int r) {
     return vec ? pick_split_rank<T, true, 3, SHRINK>(r) : pick_split_rank<T, false, 3, SHRINK>(r);
 }
 
-static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
-
-// -1 automatic, 0 SIMT only, 1 tensor cores only (env PREFT_SPLIT_VARIANT=simt|tc)
-static int g_split_variant = -2;
-int split_variant() {
-    if (g_split_variant == -2) {
-        const char* env = getenv("PREFT_SPLIT_VARIANT");
-        g_split_variant = (env && env[0] == 's') ? 0 : (env && env[0] == 't') ? 1 : -1;
-    }
-    return g_split_variant;
-}
-void set_split_variant(int v) { g_split_variant = v; }
-
 bool pdl_enabled();
 
 template <typename K>
@@ -830,6 +817,48 @@ static int fill_common(SplitArgs& args, const preft_meta_t* meta, const preft_lo
 static long long* g_split_prof = nullptr;
 void split_set_profile(long long* buf) { g_split_prof = buf; }
 
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+// -1 automatic, 0 SIMT only, 1 tensor cores only (env PREFT_SPLIT_VARIANT=simt|tc)
+static int g_split_variant = -2;
+int split_variant() {
+    if (g_split_variant == -2) {
+        const char* env = getenv("PREFT_SPLIT_VARIANT");
+        g_split_variant = (env && env[0] == 's') ? 0 : (env && env[0] == 't') ? 1 : -1;
+    }
+    return g_split_variant;
+}
+void set_split_variant(int v) { g_split_variant = v; }
+
+// Can the tcgen05 pair (shrink + expand) run this group?  Shared by the split
+// entry points and by lora_apply's r >= 16 route.
+static bool shrink_tc_ok(const preft_meta_t* meta, const void* x, long long ldx, int m,
+                         const preft_lora_site_t* sites, int nsites, int r, int dtype, const void* P, long long ldp) {
+    bool ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && m % (64 * kPps) == 0 && ldx % 8 == 0 &&
+              ldp % 4 == 0 && al16(x) && al16(P) && meta->chunks && meta->units && nsites * r <= 64;
+    for (int s = 0; s < nsites; ++s) ok = ok && sites[s].A && al16(sites[s].A);
+    return ok;
+}
+
+static bool expand_tc_ok(const preft_meta_t* meta, const void* P, long long ldp, const preft_lora_site_t* sites,
+                         int nsites, int r, int dtype) {
+    bool ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && ldp % 4 == 0 && al16(P) && meta->chunks &&
+              meta->units && nsites * r <= 64;
+    for (int s = 0; s < nsites; ++s)
+        ok = ok && sites[s].Bt_tc && sites[s].n % kSpN == 0 && sites[s].ldy % 8 == 0 && al16(sites[s].y) &&
+             al16(sites[s].Bt_tc);
+    return ok;
+}
+
+bool lora_tc_route_ok(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
+                      int nsites, int r, int dtype) {
+    if (!meta->lora_part || split_variant() == 0) return false;
+    const long long ldp = static_cast<long long>(nsites) * r;
+    if (meta->lora_part_floats < static_cast<long long>(meta->T_cap) * ldp) return false;
+    return shrink_tc_ok(meta, x, ldx, m, sites, nsites, r, dtype, meta->lora_part, ldp) &&
+           expand_tc_ok(meta, meta->lora_part, ldp, sites, nsites, r, dtype);
+}
+
 int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
                 const preft_lora_site_t* sites, int nsites, int r, int dtype, void* P, long long ldp,
                 cudaStream_t stream, int num_sms) {
@@ -845,9 +874,7 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
     args.m = m;
     fill_common(args, meta, sites, nsites, P, ldp);
     const int variant = split_variant();
-    bool tc_ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && m % (64 * kPps) == 0 && ldx % 8 == 0 && ldp % 4 == 0 &&
-                 al16(x) && al16(P) && meta->chunks && meta->units;
-    for (int s = 0; s < nsites; ++s) tc_ok = tc_ok && al16(sites[s].A);
+    const bool tc_ok = shrink_tc_ok(meta, x, ldx, m, sites, nsites, r, dtype, P, ldp);
     if (variant == 1 && !tc_ok) return PREFT_ERR_SHAPE;
     if (variant != 0 && tc_ok) {
         SplitMaps maps{};
@@ -900,11 +927,7 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
     SplitArgs args{};
     fill_common(args, meta, sites, nsites, const_cast<void*>(P), ldp);
     const int variant = split_variant();
-    bool tc_ok = dtype == PREFT_DTYPE_BF16 && (r == 16 || r == 32) && ldp % 4 == 0 && al16(P) && meta->chunks &&
-                 meta->units;
-    for (int s = 0; s < nsites; ++s)
-        tc_ok = tc_ok && sites[s].Bt_tc && sites[s].n % kSpN == 0 && sites[s].ldy % 8 == 0 && al16(sites[s].y) &&
-                al16(sites[s].Bt_tc);
+    const bool tc_ok = expand_tc_ok(meta, P, ldp, sites, nsites, r, dtype);
     if (variant == 1 && !tc_ok) return PREFT_ERR_SHAPE;
     if (variant != 0 && tc_ok) {
         SplitMaps maps{};

@@ -77,6 +77,15 @@ int preft_plan_set_rows_hint(preft_plan* p, int32_t rows) {
     return PREFT_OK;
 }
 
+int preft_plan_refresh_meta(preft_plan* p, const preft_meta_t* meta) {
+    if (!p || !meta) return PREFT_ERR_STATE;
+    const int32_t split = p->meta.slot_split, hint = p->meta.rows_hint;
+    p->meta = *meta;
+    p->meta.slot_split = split;
+    p->meta.rows_hint = hint;
+    return PREFT_OK;
+}
+
 int preft_plan_add_lora(preft_plan* p, const void* x, int64_t ldx, int32_t m, const preft_lora_site_t* sites,
                         int32_t nsites, int32_t r_max, int32_t dtype, int32_t tag) {
     if (!p || !sites || nsites < 1 || nsites > 3) return PREFT_ERR_SHAPE;

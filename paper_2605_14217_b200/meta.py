@@ -119,7 +119,10 @@ class BatchMeta:
             self.units.data_ptr(),
             self.chunk_cap,
             0,
+            None,
+            0,
         )
+        self.lora_part: torch.Tensor | None = None
         self.E = 0
         self.T = 0
         self.uniform: bool | None = None
@@ -143,6 +146,15 @@ class BatchMeta:
         qsl, slots, flags = pack_entries(batch, slot_of)
         self.uniform = mask_uniform(batch)
         return self.build_arrays(qsl, slots, flags, stream, slot_split=slot_split)
+
+    def ensure_lora_part(self) -> None:
+        """Attach the f32 workspace [T_cap][<= 64] the tensor-core LoRA route
+        keeps the rank-r intermediate in (allocated once, fixed address, so
+        plans and captured graphs stay valid)."""
+        if self.lora_part is None:
+            self.lora_part = torch.zeros(self.T_cap * 64, dtype=torch.float32, device=self.device)
+            self.c.lora_part = self.lora_part.data_ptr()
+            self.c.lora_part_floats = self.lora_part.numel()
 
     def set_slot_split(self, split: int) -> None:
         """First ReFT-class slot (AdapterPool.slot_split) for the NEXT K1 run;

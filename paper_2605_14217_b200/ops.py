@@ -107,6 +107,12 @@ def check_reft(h, meta_rows: int, pool: AdapterPool, layer: int) -> None:
     _check_act(h, "h", pool.d_model, meta_rows, pool.dtype, pool.device)
 
 
+def wants_lora_part(pool: AdapterPool) -> bool:
+    """bf16 pools of rank 16/32 run LoRA on tensor cores (preft_lora_apply's
+    tcgen05 route), which needs the meta's rank-r workspace."""
+    return pool.dtype == torch.bfloat16 and pool.lora_rank in (16, 32)
+
+
 def lora_site_array(ys, pool: AdapterPool, layer: int, sites: Sequence[str]):
     arr = (_lib.PreftLoraSite * 3)()
     for i, (name, y) in enumerate(zip(sites, ys)):
@@ -138,6 +144,8 @@ def apply_lora_group_(
     m = check_lora_group(ys, x, meta.T, pool, layer, sites)
     s = _stream(stream, pool.device)
     meta.require_split(pool.slot_split)
+    if wants_lora_part(pool):
+        meta.ensure_lora_part()
     lib = _lib.load()
     for lo, hi in lora_site_chunks(sites, pool.lora_rank):
         arr = lora_site_array(ys[lo:hi], pool, layer, sites[lo:hi])

@@ -19,7 +19,7 @@ import torch
 from . import _lib
 from .errors import ShapeError
 from .meta import BatchMeta
-from .ops import check_lora_group, check_reft, lora_site_array, lora_site_chunks, row_stride
+from .ops import check_lora_group, check_reft, lora_site_array, lora_site_chunks, row_stride, wants_lora_part
 from .pool import AdapterPool
 
 __all__ = ["StepPlan"]
@@ -64,6 +64,9 @@ class StepPlan:
         for one launch becomes several)."""
         pool = self.pool
         m = check_lora_group(ys, x, self.rows, pool, layer, sites)
+        if wants_lora_part(pool) and self.meta.lora_part is None:
+            self.meta.ensure_lora_part()
+            _lib.check(self.lib.preft_plan_refresh_meta(self.handle, ctypes.byref(self.meta.c)), "plan_refresh_meta")
         for lo, hi in lora_site_chunks(sites, pool.lora_rank):
             arr = lora_site_array(ys[lo:hi], pool, layer, sites[lo:hi])
             st = self.lib.preft_plan_add_lora(self.handle, ctypes.c_void_p(x.data_ptr()), row_stride(x), m, arr,
@@ -104,12 +107,12 @@ class StepPlan:
                    "plan_collect_timing")
         return total.value, count.value
 
-    def run(self, stream=None, run_meta: bool = True) -> None:
+    def run(self, stream=None, run_meta: bool = True, _capturing: bool = False) -> None:
         """Issue the step.  run_meta=True re-runs K1 (with the pool's slot
         split) on the entries already staged in the meta; run_meta=False
         trusts the caller's build, which must have used the pool's split."""
         s = stream if stream is not None else torch.cuda.current_stream(self.pool.device)
-        if not run_meta:
+        if not run_meta and not _capturing:
             self.meta.require_split(self.pool.slot_split)
         if not self._fixed_hint and self.meta.c.rows_hint > 0 and self.meta.c.rows_hint != self.rows_hint:
             self.set_rows_hint(self.meta.c.rows_hint)
@@ -124,11 +127,13 @@ class StepPlan:
         replay, and the kernels read the new token counts from device memory."""
         s = stream if stream is not None else torch.cuda.Stream(self.pool.device)
         s.wait_stream(torch.cuda.current_stream(self.pool.device))
+        # the graph is replayed after later builds (run_meta=False: the caller's
+        # build_arrays with slot_split=pool.slot_split before every replay)
         with torch.cuda.stream(s):
-            self.run(s, run_meta)  # warm-up: occupancy queries, smem attributes
+            self.run(s, run_meta, _capturing=True)  # warm-up: occupancy queries, smem attributes
         torch.cuda.current_stream(self.pool.device).wait_stream(s)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=s):
-            self.run(s, run_meta)
+            self.run(s, run_meta, _capturing=True)
         self.graph = g
         return g

@@ -229,3 +229,68 @@ def test_errors_map_to_reference_exceptions(cuda_device):
         apply_lora_(torch.zeros(3, 64, device=cuda_device, dtype=torch.bfloat16), x, meta, pool, 0, "Wq")
     with pytest.raises(ShapeError):
         apply_lora_(torch.zeros(2, 64, device=cuda_device), x, meta, pool, 0, "Wq")
+
+
+TC_SITES = {"Wq": (512, 512), "Wk": (128, 512), "Wv": (128, 512), "Wo": (512, 512), "Wgate": (1024, 512),
+            "Wup": (1024, 512), "Wdown": (512, 1024)}
+
+
+@pytest.mark.parametrize("variant", [-1, 0])
+@pytest.mark.parametrize("rank", [16, 32])
+def test_rank16_32_tensor_core_route(cuda_device, variant, rank):
+    """bf16 LoRA^P at r = 16 / 32 through the standard apply API: the tcgen05
+    split pair (shrink into the meta's workspace, then expand) when eligible
+    (variant -1), the SIMT kernels when forced (variant 0); both against the
+    oracle, with mixed ranks, decode entries and adapter-less entries, every
+    group of a (narrow) Llama layer, and through a StepPlan + CUDA graph."""
+    from paper_2605_14217_b200 import _lib, shapes
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_group_
+    from paper_2605_14217_b200.plan import StepPlan
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(rank + variant)
+    pool = AdapterPool(2, 512, lora_sites=TC_SITES, lora_capacity=10, lora_rank=rank, dtype=torch.bfloat16,
+                       device=cuda_device)
+    for aid in range(10):
+        pool.register(U.random_lora_adapter(rng, aid, 2, TC_SITES, rank if aid % 3 else rank // 2))
+    meta = BatchMeta(128, 4096, device=cuda_device)
+    qsl, ids, flags = U.random_entries(rng, 70, list(range(10)), max_len=90)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    T = int(qsl[-1])
+    mask = U.oracle_mask(qsl, slots, flags)
+    lib = _lib.load()
+    assert lib.preft_set_lora_variant(variant) == 0
+    try:
+        acts = {}
+        for group in shapes.SITE_GROUPS:
+            x = U.rand_act(rng, T, TC_SITES[group[0]][1], torch.bfloat16, cuda_device)
+            ys = [U.rand_act(rng, T, TC_SITES[s][0], torch.bfloat16, cuda_device) for s in group]
+            acts[group] = (x, ys, [U.to_np(y) for y in ys])
+            apply_lora_group_(ys, x, meta, pool, 1, group)
+        torch.cuda.synchronize()
+        assert meta.lora_part is not None  # the workspace the TC route uses
+        for group, (x, ys, y_in) in acts.items():
+            for s, y, yi in zip(group, ys, y_in):
+                out = U.to_np(y)
+                assert np.array_equal(out[~mask], yi[~mask])
+                ref = U.lora_oracle(yi, U.to_np(x), qsl, slots, flags, pool, 1, s)
+                helpers.check_close(out, yi, ref, "bf16", f"r={rank} variant={variant} {s}")
+        # the same through a plan replayed from a CUDA graph: equal to the per-call API bit for bit
+        base = {g: [y.clone() for y in ys] for g, (x, ys, _) in acts.items()}
+        plan = StepPlan(meta, pool, max_tokens=T)
+        for group, (x, ys, _) in acts.items():
+            plan.add_lora_group(ys, x, 0, group)
+        graph = plan.capture(run_meta=False)
+        for g, (x, ys, _) in acts.items():
+            for y, b in zip(ys, base[g]):
+                y.copy_(b)
+        graph.replay()
+        torch.cuda.synchronize()
+        for group, (x, ys, _) in acts.items():
+            want = [b.clone() for b in base[group]]
+            apply_lora_group_(want, x, meta, pool, 0, group)
+            for y, w in zip(ys, want):
+                assert torch.equal(y, w)
+    finally:
+        lib.preft_set_lora_variant(-1)
