@@ -651,8 +651,14 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                 tc::mbar_wait(&full[stage], phase);
                 tc::fence_after_sync();
                 uint32_t v[2][32];
+                // both loads unconditionally, then the wait: a tcgen05.ld whose
+                // issue sits under a branch lets the compiler merge its output
+                // registers at the join BEFORE tcgen05.wait::ld, i.e. copy
+                // registers the load has not written yet (found as stale D
+                // columns 120-127 of 256-wide chunks).  For 128-wide chunks the
+                // second load reads the other half's columns and is ignored.
                 tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpNMax + hf * (cw / 2), v[0]);
-                if (npw == 2) tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpNMax + hf * (cw / 2) + 64, v[1]);
+                tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpNMax + hf * (cw / 2) + 64, v[1]);
                 tc::tmem_ld_wait();
                 tc::fence_before_sync();
                 __syncwarp();

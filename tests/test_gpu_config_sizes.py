@@ -162,3 +162,30 @@ def test_config5_zipf_loreft_r32_long_prompts(cuda_device, variant):
 
         ref = hi + O.delta_rows(p["kind"], p["s"], hi, A=p["A"], B=p["B"], b=p["b"])
         helpers.check_close(ho, hi, ref, "bf16", f"cfg5 prompt {i} ({e - b} tokens, slot {int(slots[i])})")
+
+
+@pytest.mark.parametrize("rank", [16, 32])
+def test_lora_tensor_core_route_cfg2_batch_8b_widths(cuda_device, rank):
+    """LoRA^P r16/32 (tcgen05 split pair) at Llama-3.1-8B widths on the full
+    cfg2 batch (~240 K1 units: several per CTA, 256-wide expand chunks), one
+    launch per group, sampled rows vs the oracle.  This is the case that
+    exposed a tcgen05.ld issued under a branch (stale D columns)."""
+    import bench
+    from paper_2605_14217_b200 import shapes
+    from paper_2605_14217_b200.ops import apply_lora_group_
+
+    args = bench.parse([])
+    ctx = bench.build_step(args, 0, 1, cuda_device, 256, 256, lora_rank=rank)
+    for layer in (0, 17):
+        for group in shapes.SITE_GROUPS:
+            if len(group) * rank > 64:
+                continue  # split into several launches by apply_lora_group_; covered by the narrow-width tests
+            x, ys = ctx["acts"][group]
+            for y in ys:
+                y.copy_(torch.randn(y.shape, device=cuda_device))
+            snap = {group: [y.clone() for y in ys]}
+            apply_lora_group_(ys, x, ctx["meta"], ctx["pool"], layer, group)
+            torch.cuda.synchronize()
+            r = bench.check_lora_accumulated(ctx["pool"], ctx["meta"], ctx["qsl"], ctx["slots"], {group: (x, ys)},
+                                             snap, [layer], k=96, seed=layer)
+            assert r["status"] == "pass", (layer, group, r)
