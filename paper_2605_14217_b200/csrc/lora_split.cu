@@ -492,7 +492,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
         // producer: lane 4*pp + q issues y panel pp of chunk q, lane 16 the Bt chunk
         const uint64_t stream = tc::policy_evict_first();
         const int pp = lane >> 2, q = lane & 3;
-        int stage = 0;
+        int stage = 0, npc = 0;
         uint32_t phase = 0;
         for (int w = it.w0; w < it.w1; ++w) {
             const int4 U = a.units[w / it.ipu];
@@ -509,8 +509,10 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                 const uint32_t bt_bytes = static_cast<uint32_t>(cw * R * 2);
                 if (lane == 0) {
                     tc::mbar_wait(&empty[stage], phase ^ 1u);
+                    if (a.prof && blockIdx.x == 0 && npc < 128) a.prof[512 + npc * 4 + 0] = clock64();
                     tc::mbar_expect_tx(&full[stage], static_cast<uint32_t>((cw / 64) * nch * kSpChunk * 128) + bt_bytes);
                 }
+                ++npc;
                 __syncwarp();
                 const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
                 if (contig) {
@@ -557,6 +559,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                     const int db = dc & 1;
                     tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
                     tc::fence_after_sync();
+                    if (a.prof && blockIdx.x == 0 && dc < 128) a.prof[512 + dc * 4 + 1] = clock64();
                     const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
                     const uint32_t dD = tmem + db * kSpNMax;
                     const uint32_t id = it.cw[s] == kSpNMax ? id256 : id128;
@@ -650,6 +653,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                 tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
                 tc::mbar_wait(&full[stage], phase);
                 tc::fence_after_sync();
+                if (a.prof && blockIdx.x == 0 && warp == 4 && lane == 0 && dc < 128) a.prof[512 + dc * 4 + 2] = clock64();
                 uint32_t v[2][32];
                 // both loads unconditionally, then the wait: a tcgen05.ld whose
                 // issue sits under a branch lets the compiler merge its output
@@ -722,6 +726,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                     tc::tma_store_wait_read_1();
                     if (pend >= 0) tc::mbar_arrive(&empty[pend]);
                     pend = stage;
+                    if (a.prof && blockIdx.x == 0 && warp == 4 && dc < 128) a.prof[512 + dc * 4 + 3] = clock64();
                 }
                 __syncwarp();
                 if (++stage == L::STAGES) {
@@ -932,6 +937,7 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
         if (!sites[s].scale || !sites[s].y || sites[s].n < 1 || sites[s].ldy < sites[s].n) return PREFT_ERR_SHAPE;
     SplitArgs args{};
     fill_common(args, meta, sites, nsites, const_cast<void*>(P), ldp);
+    args.prof = g_split_prof;
     const int variant = split_variant();
     const bool tc_ok = expand_tc_ok(meta, P, ldp, sites, nsites, r, dtype);
     if (variant == 1 && !tc_ok) return PREFT_ERR_SHAPE;
