@@ -83,6 +83,8 @@ extern "C" {
 #define PREFT_CTR_SPLIT 7       /* selected tokens whose slot < slot_split  */
 #define PREFT_CTR_CHUNKS 8      /* row chunks (<= PREFT_CHUNK_ROWS rows of one entry) */
 #define PREFT_CTR_UNITS 9       /* tensor-core work units (<= 4 chunks of one slot)  */
+#define PREFT_CTR_LORA_UNITS 10 /* units whose slot < slot_split (they come first)   */
+#define PREFT_CTR_LORA_CHUNKS 11 /* chunks of those units (they come first as well)   */
 #define PREFT_NUM_COUNTERS 12
 
 /* rows per chunk: one TMA box / one TMEM lane quadrant of an M = 64 UMMA */
@@ -223,11 +225,18 @@ int preft_lora_shrink(const preft_meta_t* meta, const void* x, int64_t rows, int
 int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int64_t rows,
                       const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype,
                       void* stream);
+/* Floats the tensor-core split wants in meta->lora_part (zero-initialised):
+ * partial planes of P for units the shrink shares between CTAs, plus one
+ * arrival counter per unit.  With less, every unit's shrink stays on one CTA. */
+int64_t preft_lora_part_floats(const preft_meta_t* meta);
 /* split-kernel variant: -1 automatic, 0 SIMT only, 1 tensor cores only
  * (PREFT_ERR_SHAPE when ineligible).  Env: PREFT_SPLIT_VARIANT=simt|tc. */
 int preft_set_split_variant(int32_t variant);
-/* Diagnostic: clock64() stamps of the tensor-core shrink's CTA 0 (4 per
- * panel / unit, 512 int64, NULL = off). */
+/* Diagnostic: clock64() stamps of CTA 0 of the tensor-core shrink (4 per
+ * stage / unit at [0, 512)) and expand (4 + 4 per item at [512, 1024) and
+ * [1024, 1536)), then per-CTA globaltimer windows of CTAs 0-127 (shrink at
+ * [1536, 1792), expand at [1792, 2048)); 2048
+ * int64, NULL = off. */
 int preft_diag_split(long long* device_buffer);
 
 /*

@@ -39,6 +39,8 @@ CTR_E = 6
 CTR_SPLIT = 7
 CTR_CHUNKS = 8
 CTR_UNITS = 9
+CTR_LORA_UNITS = 10
+CTR_LORA_CHUNKS = 11
 NUM_COUNTERS = 12
 CHUNK_ROWS = 16
 UNIT_CHUNKS = 4
@@ -157,6 +159,7 @@ SIGNATURES = {
     ),
     "preft_set_split_variant": (ctypes.c_int, [ctypes.c_int32]),
     "preft_diag_split": (ctypes.c_int, [ctypes.c_void_p]),
+    "preft_lora_part_floats": (ctypes.c_int64, [ctypes.POINTER(PreftMeta)]),
     "preft_diag_reft_tc": (ctypes.c_int, [ctypes.c_void_p]),
     "preft_convert_2d": (
         ctypes.c_int,

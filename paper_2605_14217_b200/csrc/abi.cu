@@ -17,6 +17,7 @@ int reft_apply(const preft_meta_t* meta, void* h, long long rows, long long ldh,
 void set_reft_variant(int v);
 void set_split_variant(int v);
 void split_set_profile(long long* buf);
+long long lora_part_floats_needed(const preft_meta_t* meta);
 int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
                 const preft_lora_site_t* sites, int nsites, int r, int dtype, void* P, long long ldp,
                 cudaStream_t stream, int num_sms);
@@ -194,6 +195,10 @@ int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int6
                       const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype, void* stream) {
     return finish(lora_expand(meta, P, ldp, rows, sites, nsites, r_max, dtype, static_cast<cudaStream_t>(stream),
                               current_num_sms()));
+}
+
+int64_t preft_lora_part_floats(const preft_meta_t* meta) {
+    return meta ? lora_part_floats_needed(meta) : 0;
 }
 
 int preft_diag_split(long long* device_buffer) {

@@ -14,11 +14,14 @@
 // never read).
 //
 // Two implementations each:
-//   tcgen05 (bf16, R in {16, 32}, m % 64 == 0, n % 128 == 0): the M = 64 unit
-//     pipeline of the tensor-core ReFT kernel (csrc/reft_tc.cu) cut in half —
-//     shrink: TMA x/A panels -> UMMA -> TMEM -> P rows;  expand: P rows ->
-//     bf16 hi/lo V -> UMMA against the pre-tiled Bt chunk -> TMEM -> y chunk
-//     read-modify-write in shared memory -> TMA store.  One CTA per SM.
+//   tcgen05 (bf16, R in {16, 32}, m % 256 == 0, n % 128 == 0): persistent
+//     warp-specialised kernels over K1's M = 64 units — shrink: TMA x/A
+//     panels -> UMMA -> TMEM -> P rows;  expand: P rows -> bf16 hi/lo V ->
+//     UMMA against the pre-tiled Bt block -> TMEM -> y tile read-modify-write
+//     in shared memory -> TMA store.  Each CTA takes a contiguous,
+//     cost-balanced range of (unit, column block) items (see item_range):
+//     with short prompts there are only ~1.6 units per SM, and whole-unit
+//     shares left the slowest CTA with 2-4x the mean work.
 //   SIMT (any dtype / rank, one warp per token row) for everything else.
 #include <cuda_bf16.h>
 
@@ -49,15 +52,18 @@ struct SplitArgs {
     SplitSite site[3];
     void* P;  // [rows][ldp] acc type
     long long ldp;
-    int slot_base;  // LoRA-class slots are < slot_base (meta->slot_split)
-    int ks;         // tensor-core shrink: K splits per unit (1 or 2)
+    int slot_base;  // LoRA-class slots are < slot_split (meta->slot_split)
+    int max_planes; // tensor-core shrink: CTAs that may share one unit (1 = whole units)
+    float* planes;  // partial planes p >= 1 at planes + p * plane_stride (row stride ldp)
+    long long plane_stride;
+    int* sync;      // per-unit arrival counters (zero between launches)
+    int flags;      // kSplitTmaStore: the expand stores full chunks by TMA (default: st.global from smem)
     long long* prof;  // diagnostics: clock64 stamps of CTA 0 (NULL in production)
     const int2* tokens;
     const int2* chunks;
     const int4* units;
     const int* counters;
 };
-
 // ---------------------------------------------------------------- SIMT halves
 
 template <typename T, bool VEC, int R, int NS, int U>
@@ -176,22 +182,23 @@ __global__ void __launch_bounds__(256) expand_simt_kernel(const SplitArgs a) {
 
 constexpr int kSpU = 64;                  // unit rows (UMMA M)
 constexpr int kSpChunk = PREFT_CHUNK_ROWS;
-constexpr int kSpN = 128;                 // expand chunk width (UMMA N) of narrow sites
-constexpr int kSpNMax = 256;              // expand chunk width of sites with n % 256 == 0
+constexpr int kSpN = 128;                 // expand block width (UMMA N) of narrow sites
+constexpr int kSpNMax = 256;              // expand block width of sites with n % 256 == 0
 constexpr int kSpAcc = 4;                 // split shrink accumulators = UMMA-issuing warps
 constexpr int kShrinkThreads = 32 * (6 + kSpAcc);
+constexpr int kPps = 4;                   // K panels (64 columns) per shrink item / ring stage
+constexpr int kPlanes = 4;                // max CTAs sharing one unit's shrink (P partial planes)
+constexpr int kSplitTmaStore = 1;
 
 struct SplitMaps {
     CUtensorMap x;       // x [rows][m] (this rank's columns), 16-row x 64-col boxes
     CUtensorMap x64;     // the same with 64-row boxes (a unit of 4 contiguous chunks)
     CUtensorMap A[3];    // A_s [S*R][m], R-row x 64-col boxes
-    CUtensorMap y[3];    // y_s [rows][n], 16-row x 64-col boxes
-    CUtensorMap y64[3];  // the same with 64-row boxes
+    CUtensorMap y[3];    // y_s as [panels][rows][64] (make_tmap_bf16_panels), box {64, 16, block/64}
 };
 
 // A unit whose 4 chunks are consecutive rows of one entry loads as ONE 64-row
-// TMA box: a TMA instruction costs ~100 cycles to issue, so per-chunk boxes
-// (4 per panel) capped the shrink at ~8 KB per 400 cycles per SM.
+// TMA box per panel (a TMA instruction costs ~30-100 cycles to issue).
 __device__ __forceinline__ bool unit_contiguous(const int2* chunks, int4 U) {
     if (U.z != 4) return false;
     const int2 c0 = chunks[U.y], c1 = chunks[U.y + 1], c2 = chunks[U.y + 2], c3 = chunks[U.y + 3];
@@ -199,7 +206,114 @@ __device__ __forceinline__ bool unit_contiguous(const int2* chunks, int4 U) {
            c2.x == c0.x + 2 * kSpChunk && c3.x == c0.x + 3 * kSpChunk;
 }
 
-constexpr int kPps = 4;  // K panels (64 columns each) per shrink ring stage: amortises the per-stage overheads
+// ---- cost-balanced work ranges
+//
+// Work items are (unit u, column block c) over the LoRA-class units (K1 lists
+// them first; counters[PREFT_CTR_LORA_UNITS]), c over `nc` blocks of a unit's
+// columns (the expand: every site's output columns; the shrink: the input
+// columns, kPps panels per block).  Item (u, c) costs
+//     width(c) * (alpha * nch_u + beta)        (bytes-equivalent)
+// alpha per column per 16-row chunk (activation traffic), beta per column
+// (the adapter's weights plus a fixed per-item overhead).  The cost ahead of
+// unit u is  W * (alpha * ch0(u) + beta * u)  with ch0(u) = units[u].y, K1's
+// exclusive prefix of chunk counts.  Each CTA takes the items whose start
+// cost falls in its 1/G of the total, found by a two-level parallel search
+// over the units — no host round trip, so the launch stays graph-safe.
+struct Blocks {
+    int nc;        // blocks per unit
+    int nsites;
+    int first[4];  // first block of each site (first[nsites] = nc)
+    int cw[3];     // block width of each site
+    int coff[3];   // first column of each site among the unit's columns
+    long long W;   // columns per unit
+    __device__ __forceinline__ int site(int c) const {
+        int s = 0;
+        while (s + 1 < nsites && c >= first[s + 1]) ++s;
+        return s;
+    }
+    __device__ __forceinline__ long long off(int c) const {
+        const int s = site(c);
+        return coff[s] + static_cast<long long>(c - first[s]) * cw[s];
+    }
+    // first block whose column offset is >= X (nc if none)
+    __device__ __forceinline__ int first_at_least(long long X) const {
+        if (X <= 0) return 0;
+        for (int s = 0; s < nsites; ++s) {
+            const long long last = coff[s] + static_cast<long long>(first[s + 1] - first[s] - 1) * cw[s];
+            if (X <= last) {
+                const long long j = (X - coff[s] + cw[s] - 1) / cw[s];
+                return first[s] + (j > 0 ? static_cast<int>(j) : 0);
+            }
+        }
+        return nc;
+    }
+};
+
+struct CostModel {
+    const int4* units;
+    int nu;
+    int nch_tot;  // chunks of the LoRA-class units (counters[PREFT_CTR_LORA_CHUNKS])
+    long long alpha, beta;
+    int G;  // CTAs sharing the items (CTAs >= G get none)
+    long long tot;
+    __device__ __forceinline__ long long prefix(int u, const Blocks& b) const {
+        const int ch0 = u < nu ? units[u].y : nch_tot;
+        return b.W * (alpha * ch0 + beta * u);
+    }
+    __device__ __forceinline__ void load(const int* counters) {
+        nu = counters[PREFT_CTR_LORA_UNITS];
+        nch_tot = counters[PREFT_CTR_LORA_CHUNKS];
+    }
+    __device__ __forceinline__ long long target(int cta) const { return tot * cta / G; }
+    // the CTA whose share holds cost position S
+    __device__ __forceinline__ int owner(long long S) const {
+        int b = static_cast<int>(S * G / tot);
+        b = b < G - 1 ? b : G - 1;
+        while (b + 1 < G && target(b + 1) <= S) ++b;
+        while (b > 0 && target(b) > S) --b;
+        return b;
+    }
+    // first item of unit u (or u + 1) whose start cost is >= t
+    __device__ __forceinline__ int first_item(int u, long long t, const Blocks& b) const {
+        const long long base = prefix(u, b), per = alpha * units[u].z + beta;
+        const long long X = t > base ? (t - base + per - 1) / per : 0;
+        return u * b.nc + b.first_at_least(X);
+    }
+};
+
+// [k0, k1) of this CTA; every thread of the block must call it
+__device__ void item_range(CostModel& cm, const Blocks& b, int* s_u, int& k0, int& k1) {
+    k0 = k1 = 0;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int nu = cm.nu;
+    if (nu <= 0) return;
+    cm.tot = cm.prefix(nu, b);
+    if (static_cast<int>(blockIdx.x) >= cm.G || cm.tot <= 0) return;
+    const long long t0 = cm.target(blockIdx.x), t1 = cm.target(blockIdx.x + 1);
+    const int step = (nu + nt - 1) / nt;
+    if (tid < 2) s_u[tid] = 0;
+    __syncthreads();
+    int u = tid * step;
+    if (u < nu) {
+        const long long p = cm.prefix(u, b);
+        if (p <= t0) atomicMax(&s_u[0], u);
+        if (p <= t1) atomicMax(&s_u[1], u);
+    }
+    __syncthreads();
+    const int l0 = s_u[0], l1 = s_u[1];
+    __syncthreads();
+    if (tid < step) {
+        u = l0 + tid;
+        if (u < nu && cm.prefix(u, b) <= t0) atomicMax(&s_u[0], u);
+        u = l1 + tid;
+        if (u < nu && cm.prefix(u, b) <= t1) atomicMax(&s_u[1], u);
+    }
+    __syncthreads();
+    k0 = cm.first_item(s_u[0], t0, b);
+    k1 = static_cast<int>(blockIdx.x) + 1 == cm.G ? nu * b.nc : cm.first_item(s_u[1], t1, b);
+}
+
+// ---- shrink
 
 template <int R, int NS>
 struct ShrinkLayout {
@@ -215,7 +329,16 @@ struct ShrinkLayout {
     static_assert(2 * kSpAcc * NSR <= 512, "TMEM budget");
 };
 
-// warps: 0 TMA producer (x), 6 TMA producer (A), 1 UMMA issuer, 2..5 TMEM -> P rows (lane quadrant = warp % 4)
+__device__ __forceinline__ void readout_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// Items are (unit, block of kPps K panels); a CTA accumulates its run of a
+// unit's blocks (a "visit") in TMEM.  When several CTAs share a unit (at most
+// max_planes), each writes its partial to plane (cta - first owner) and the
+// last to arrive sums the planes in plane order into P — a fixed summation
+// order, so results do not depend on which CTA finishes last.
+//
+// warps: 0 TMA producer (x), 6 TMA producer (A), 1 + 7..9 UMMA issuers,
+//        2..5 TMEM -> P rows (lane quadrant = warp % 4)
 template <int R, int NS>
 __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
     using L = ShrinkLayout<R, NS>;
@@ -223,6 +346,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
     __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
     __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
     __shared__ uint32_t tslot;
+    __shared__ int s_u[2];
+    __shared__ int s_last;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t sbase = (tc::smem_u32(sm_raw) + 1023u) & ~1023u;
     if (warp == 0) tc::tmem_alloc(&tslot, L::TMEM_COLS);
@@ -242,31 +367,66 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
     __syncthreads();
     tc::fence_after_sync();
     const uint32_t tmem = tslot;
-    // work item = (unit, 1/ks of the K panels): ks = 2 balances launches with
-    // ~2 units per SM; the two halves meet in P through f32 atomics, whose
-    // order cannot change a two-term sum (0 + a + b == 0 + b + a)
     tc::pdl_launch_dependents();
-    tc::pdl_wait();  // everything below reads the previous kernels' output
-    const int ks = a.ks;
-    int w0, w1;
-    even_share(a.counters[PREFT_CTR_UNITS] * ks, blockIdx.x, gridDim.x, w0, w1);
+
+    // K blocks of kPps panels; with one plane a unit is never split
     const int NP = a.m / 64;
+    Blocks bl;
+    bl.nsites = 1;
+    bl.nc = a.max_planes > 1 ? NP / kPps : 1;
+    bl.cw[0] = bl.nc == 1 ? a.m : 64 * kPps;
+    bl.coff[0] = 0;
+    bl.first[0] = 0;
+    bl.first[1] = bl.nc;
+    bl.W = a.m;
+    CostModel cm;
+    cm.units = a.units;
+    cm.load(a.counters);
+    cm.alpha = kSpChunk * 2;                   // x bytes per column per chunk
+    cm.beta = NS * R * 2 + 16;                 // A bytes per column + per-item overhead
+    cm.G = gridDim.x;
+    if (a.max_planes > 1 && cm.nu > 0) {
+        // a unit may span at most max_planes CTAs: cap the CTAs sharing the
+        // work so that one CTA's share is >= max_unit / f, f = max(1,
+        // max_planes - 2) (a unit then meets at most f + 1 CTAs, with one
+        // to spare for the rounding of the share boundaries)
+        const long long tot = cm.prefix(cm.nu, bl);
+        const long long umax = bl.W * (cm.alpha * PREFT_UNIT_CHUNKS + cm.beta);
+        const long long f = a.max_planes > 3 ? a.max_planes - 2 : 1;
+        const long long g = f * tot / umax;
+        cm.G = static_cast<int>(g < 1 ? 1 : g < cm.G ? g : cm.G);
+    }
+    int k0, k1;
+    // the schedule reads only K1's units and counters, written by a meta
+    // build that completed before the first kernel of this PDL chain could
+    // start (K1 never triggers its dependents early), so it is found while the
+    // previous kernel drains; x, A and P are touched only after the wait
+    item_range(cm, bl, s_u, k0, k1);
+    const int nc = bl.nc;
+    tc::pdl_wait();
+    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1536 + 2 * blockIdx.x] = tc::globaltimer();
 
     if (warp == 0) {
-        // x producer: lane q issues chunk q's box, so a stage's boxes are in
-        // flight together (one thread pays ~100+ cycles per TMA issue)
+        // x producer: lane q issues chunk q's boxes, so a stage's boxes are in
+        // flight together
         const uint64_t stream = tc::policy_evict_first();
-        int stage = 0, npf = 0;
+        int stage = 0, npf = 0, pu = -1, row = 0, r0 = 0, nch = 0;
+        bool contig = false;
         uint32_t phase = 0;
-        for (int w = w0; w < w1; ++w) {
-            const int4 U = a.units[w / ks];
-            if (U.x >= a.slot_base) continue;  // ReFT-class unit
-            const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
-            const int nch = U.z;
-            const int row = lane < nch ? a.chunks[U.y + lane].x : 0;
-            const bool contig = unit_contiguous(a.chunks, U);
+        for (int k = k0; k < k1; ++k) {
+            const int u = k / nc, g = k - u * nc;
+            if (u != pu) {
+                const int4 U = a.units[u];
+                nch = U.z;
+                row = lane < nch ? a.chunks[U.y + lane].x : 0;
+                r0 = __shfl_sync(0xffffffffu, row, 0);
+                contig = unit_contiguous(a.chunks, U);
+                pu = u;
+            }
+            const int p = g * (bl.cw[0] / 64);
+            const int np = bl.cw[0] / 64;
             const uint32_t bytes = static_cast<uint32_t>(kPps * (nch * kSpChunk * 128 + NS * L::AP_BYTES));
-            for (int p = p0; p < p1; p += kPps) {
+            for (int pi = 0; pi < np; pi += kPps) {
                 if (lane == 0) {
                     tc::mbar_wait(&empty[stage], phase ^ 1u);
                     if (a.prof && blockIdx.x == 0 && npf < 128) a.prof[npf * 4 + 0] = clock64();
@@ -274,16 +434,16 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
                 }
                 __syncwarp();
                 const uint32_t st = sbase + stage * L::STAGE;
-                const int rq = __shfl_sync(0xffffffffu, row, lane & 3);  // chunk (lane & 3)'s first row, all lanes
-                const int r0 = __shfl_sync(0xffffffffu, row, 0);         // the unit's first row
+                const int rq = __shfl_sync(0xffffffffu, row, lane & 3);  // chunk (lane & 3)'s first row
                 if (contig) {
                     if (lane < kPps)
-                        tc::tma_load_2d_hint(st + lane * L::PANEL, &maps.x64, (p + lane) * 64, r0, &full[stage], stream);
+                        tc::tma_load_2d_hint(st + lane * L::PANEL, &maps.x64, (p + pi + lane) * 64, r0, &full[stage],
+                                             stream);
                 } else if (lane < 4 * kPps) {
                     const int pp = lane >> 2, q = lane & 3;
                     if (q < nch)
-                        tc::tma_load_2d_hint(st + pp * L::PANEL + q * (kSpChunk * 128), &maps.x, (p + pp) * 64, rq,
-                                             &full[stage], stream);
+                        tc::tma_load_2d_hint(st + pp * L::PANEL + q * (kSpChunk * 128), &maps.x, (p + pi + pp) * 64,
+                                             rq, &full[stage], stream);
                 }
                 ++npf;
                 if (++stage == L::STAGES) {
@@ -293,24 +453,26 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             }
         }
     } else if (warp == 6) {
-        // second producer: the adapters' A panels (TMA issue costs ~100+ cycles
-        // per box from one thread, so x and A boxes are issued from two warps)
+        // second producer: the adapters' A panels
         if (lane == 0) {
-            int stage = 0;
+            int stage = 0, pu = -1, slot = 0;
             uint32_t phase = 0;
-            for (int w = w0; w < w1; ++w) {
-                const int4 U = a.units[w / ks];
-                if (U.x >= a.slot_base) continue;
-                const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
-                for (int p = p0; p < p1; p += kPps) {
+            for (int k = k0; k < k1; ++k) {
+                const int u = k / nc, g = k - u * nc;
+                if (u != pu) {
+                    slot = a.units[u].x;
+                    pu = u;
+                }
+                const int np = bl.cw[0] / 64, p = g * np;
+                for (int pi = 0; pi < np; pi += kPps) {
                     tc::mbar_wait(&empty[stage], phase ^ 1u);
                     const uint32_t st = sbase + stage * L::STAGE;
 #pragma unroll
                     for (int pp = 0; pp < kPps; ++pp)
 #pragma unroll
                         for (int s = 0; s < NS; ++s)
-                            tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s], (p + pp) * 64,
-                                            U.x * R, &full[stage]);
+                            tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s],
+                                            (p + pi + pp) * 64, slot * R, &full[stage]);
                     if (++stage == L::STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -319,54 +481,69 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             }
         }
     } else if (warp == 1 || warp >= 7) {
-        // kSpAcc warps issue the UMMAs, K-step k into accumulator k % kSpAcc:
-        // one issuing thread is capped at ~140 cycles per UMMA
+        // kSpAcc warps issue the UMMAs, K-step k into accumulator k % kSpAcc
         const int mw = warp == 1 ? 0 : warp - 6;
         if (lane == 0) {
             // the sites' A panels sit back to back in the stage, so one UMMA with
-            // N = NS * R covers all of them (tiny-N UMMAs cost ~60-90 cycles each)
+            // N = NS * R covers all of them
             const uint32_t id = tc::idesc_bf16_f32(kSpU, L::NSR);
-            int stage = 0, ub = 0, nmc = 0;
+            int stage = 0, ub = 0, nmc = 0, kk = 0;
             uint32_t phase = 0;
-            for (int w = w0; w < w1; ++w) {
-                const int4 U = a.units[w / ks];
-                if (U.x >= a.slot_base) continue;
-                const int p0 = (w % ks) * NP / ks, p1 = (w % ks + 1) * NP / ks;
+            for (int k = k0; k < k1; ++k) {
+                const int u = k / nc;
+                const bool first = k == k0 || (k - 1) / nc != u;
+                const bool last = k + 1 == k1 || (k + 1) / nc != u;
                 const int sb = ub & 1;
-                tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
-                tc::fence_after_sync();
                 const uint32_t dS = tmem + sb * kSpAcc * L::NSR;
-                for (int p = p0; p < p1; p += kPps) {
+                if (first) {
+                    tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
+                    tc::fence_after_sync();
+                    kk = 0;
+                }
+                const int np = bl.cw[0] / 64;
+                for (int pi = 0; pi < np; pi += kPps) {
                     tc::mbar_wait(&full[stage], phase);
                     if (a.prof && blockIdx.x == 0 && mw == 0 && nmc < 128) a.prof[nmc * 4 + 1] = clock64();
                     ++nmc;
                     tc::fence_after_sync();
                     const uint32_t st = sbase + stage * L::STAGE;
 #pragma unroll
-                    for (int k = mw; k < 4 * kPps; k += kSpAcc) {
-                        const int kk = (p - p0) * 4 + k, pp = k >> 2, kq = k & 3;
+                    for (int j = mw; j < 4 * kPps; j += kSpAcc) {
+                        const int pp = j >> 2, kq = j & 3;
                         tc::mma_bf16(dS + mw * L::NSR, tc::desc_kmajor_sw128(st + pp * L::PANEL + kq * 32),
                                      tc::desc_kmajor_sw128(st + L::X_BYTES + pp * NS * L::AP_BYTES + kq * 32), id,
-                                     kk >= kSpAcc ? 1u : 0u);
+                                     kk + j >= kSpAcc ? 1u : 0u);
                     }
+                    kk += 4 * kPps;
                     tc::mma_commit(&empty[stage]);
                     if (++stage == L::STAGES) {
                         stage = 0;
                         phase ^= 1u;
                     }
                 }
-                tc::mma_commit(&s_full[sb]);
-                ++ub;
+                if (last) {
+                    tc::mma_commit(&s_full[sb]);
+                    ++ub;
+                }
             }
         }
     } else if (warp < 6) {
         const int q = warp & 3;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         int ub = 0;
-        for (int w = w0; w < w1; ++w) {
-            const int4 U = a.units[w / ks];
-            if (U.x >= a.slot_base) continue;
+        for (int k = k0; k < k1; ++k) {
+            const int u = k / nc;
+            if (!(k + 1 == k1 || (k + 1) / nc != u)) continue;  // act once per visit, at its last item
+            const int4 U = a.units[u];
             const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
+            // which plane: this CTA's index among the CTAs sharing the unit
+            int plane = 0, np = 1;
+            if (nc > 1) {
+                const long long base = cm.prefix(u, bl), per = cm.alpha * U.z + cm.beta;
+                const int c_first = cm.owner(base), c_last = cm.owner(base + bl.off(nc - 1) * per);
+                plane = static_cast<int>(blockIdx.x) - c_first;
+                np = c_last - c_first + 1;
+            }
             const int sb = ub & 1;
             tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
             if (a.prof && blockIdx.x == 0 && lane == 0 && q == 0 && ub < 128) a.prof[ub * 4 + 2] = clock64();
@@ -387,80 +564,116 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+            float* P0 = static_cast<float*>(a.P);
+            float* dst = plane == 0 ? P0 : a.planes + plane * a.plane_stride;
             if (lane < ch.y) {
-                float* pr = static_cast<float*>(a.P) + static_cast<long long>(ch.x + lane) * a.ldp;
-                if (ks == 1) {
+                float* pr = dst + static_cast<long long>(ch.x + lane) * a.ldp;
 #pragma unroll
-                    for (int c = 0; c < L::NSR; c += 4)
-                        *reinterpret_cast<float4*>(pr + c) = make_float4(s[c], s[c + 1], s[c + 2], s[c + 3]);
-                } else {
-#pragma unroll
-                    for (int c = 0; c < L::NSR; ++c) atomicAdd(pr + c, s[c]);
+                for (int c = 0; c < L::NSR; c += 4)
+                    *reinterpret_cast<float4*>(pr + c) = make_float4(s[c], s[c + 1], s[c + 2], s[c + 3]);
+            }
+            if (np > 1) {
+                // arrive (the CUDA threadFenceReduction pattern: the barrier
+                // orders the four warps' plane rows before one thread's fence
+                // + atomic); the last of the unit's np CTAs sums the planes
+                readout_bar();
+                if (warp == 2 && lane == 0) {
+                    __threadfence();
+                    s_last = atomicAdd(a.sync + u, 1) == np - 1;
+                    if (s_last) __threadfence();
                 }
+                readout_bar();
+                if (s_last) {
+                    if (lane < ch.y) {
+                        const long long row = static_cast<long long>(ch.x + lane) * a.ldp;
+#pragma unroll
+                        for (int c = 0; c < L::NSR; c += 4) {
+                            float4 v = __ldcg(reinterpret_cast<const float4*>(P0 + row + c));
+                            for (int p = 1; p < np; ++p) {
+                                const float4 w = __ldcg(reinterpret_cast<const float4*>(a.planes + p * a.plane_stride + row + c));
+                                v.x += w.x;
+                                v.y += w.y;
+                                v.z += w.z;
+                                v.w += w.w;
+                            }
+                            *reinterpret_cast<float4*>(P0 + row + c) = v;
+                        }
+                    }
+                    if (warp == 2 && lane == 0) a.sync[u] = 0;  // every contributor has arrived
+                }
+                readout_bar();  // s_last is rewritten by the next visit
             }
             ++ub;
         }
     }
     tc::fence_before_sync();
     __syncthreads();
+    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1537 + 2 * blockIdx.x] = tc::globaltimer();
     if (warp == 0) {
         __syncwarp();
         tc::tmem_dealloc(tmem, L::TMEM_COLS);
     }
 }
 
-template <int R, int NS>
+// ---- expand
+
+// EPI = kEpiRmw: y rows come into the ring by TMA, the epilogue adds D in
+// shared memory and stores the rows back.  EPI = kEpiReduce: the ring holds
+// only Bt; the epilogue writes bf16(D) into a staging tile and a TMA
+// reduce-add adds it into y in L2 (rows of a partial chunk beyond the
+// entry's own are padded with -0.0, which leaves any value and the sign of
+// zero unchanged), so y never passes through the SM.
+constexpr int kEpiRmw = 0, kEpiReduce = 1;
+
+template <int R, int NS, int EPI>
 struct ExpandLayout {
-    static constexpr int Y_BYTES = 4 * kSpU * 128;         // 64 rows x 256 cols (four swizzled panels)
+    static constexpr int QS = 4 * kSpChunk * 128;         // one chunk's rows of a block: <= 4 panels x 16 rows x 128 B
+    static constexpr int Y_BYTES = EPI == kEpiRmw ? 4 * QS : 0;  // the y rows of 4 chunks (32 KB)
     static constexpr int BT_BYTES = kSpNMax * R * 2;
-    static constexpr int STAGE = Y_BYTES + BT_BYTES;       // multiple of 1024
-    static constexpr int V_BYTES = kSpU * R * 2;           // one V (hi or lo) of one site
-    static constexpr int OFF_V = 0;                        // [2 buffers][NS sites][hi, lo]
-    static constexpr int OFF_RING = 4 * NS * V_BYTES;      // multiple of 1024
+    static constexpr int STAGE = Y_BYTES + BT_BYTES;      // multiple of 1024
+    static constexpr int V_BYTES = kSpU * R * 2;          // one V (hi or lo) of one site
+    static constexpr int OFF_V = 0;                       // [2 buffers][NS sites][hi, lo]
+    static constexpr int OFF_STG = 4 * NS * V_BYTES;      // reduce staging [2 groups][2 buffers][4 chunks] x QS
+    static constexpr int STG_BYTES = EPI == kEpiReduce ? 2 * 2 * 4 * QS : 0;
+    static constexpr int OFF_RING = OFF_STG + STG_BYTES;  // multiple of 1024
     static constexpr int STAGES_FIT = (227 * 1024 - 2048 - OFF_RING) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
     static constexpr int SMEM = OFF_RING + STAGES * STAGE + 1024;
     static_assert(STAGES >= 3, "expand ring too shallow");
 };
 
-// The expand's work item is (unit, block of kExpBlock 128-column chunks) over
-// the concatenated chunks of all sites, so a launch balances across CTAs even
-// when a batch has few units per SM (Punica-sized steps: ~2 units per CTA,
-// but 56 gate/up chunks per unit).  Consecutive items of one unit share its V.
-constexpr int kExpBlock = 4;
-
-struct ExpandItems {
-    int w0, w1;  // this CTA's contiguous share of items
-    int ipu;     // items per unit
-    int nc;      // chunks per unit (all sites)
-    int off[4];  // first chunk of each site
-    int cw[3];   // chunk width of each site: 256 columns (one N = 256 UMMA), else 128
-    __device__ void init(const SplitArgs& a, int nsites) {
-        nc = 0;
-        for (int s = 0; s < nsites; ++s) {
-            off[s] = nc;
-            cw[s] = a.site[s].n % kSpNMax == 0 ? kSpNMax : kSpN;
-            nc += a.site[s].n / cw[s];
-        }
-        off[nsites] = nc;
-        ipu = (nc + kExpBlock - 1) / kExpBlock;
-        even_share(a.counters[PREFT_CTR_UNITS] * ipu, blockIdx.x, gridDim.x, w0, w1);
+__device__ __forceinline__ void expand_blocks(Blocks& b, const SplitArgs& a, int nsites) {
+    b.nsites = nsites;
+    b.nc = 0;
+    long long W = 0;
+    for (int s = 0; s < nsites; ++s) {
+        b.first[s] = b.nc;
+        b.cw[s] = a.site[s].n % kSpNMax == 0 ? kSpNMax : kSpN;
+        b.coff[s] = static_cast<int>(W);
+        b.nc += a.site[s].n / b.cw[s];
+        W += a.site[s].n;
     }
-    __device__ void site_of(int c, int nsites, int& s, int& j) const {
-        s = 0;
-        while (s + 1 < nsites && c >= off[s + 1]) ++s;
-        j = c - off[s];
-    }
-};
+    b.first[nsites] = b.nc;
+    b.W = W;
+}
 
-// warps: 0 TMA producer, 1 UMMA issuer, 2-3 P rows -> bf16 hi/lo V, 4-11 epilogue
-template <int R, int NS>
+// Items are (unit, output block): per item the producer loads the unit's y
+// rows of the block with one 3D TMA box per 16-row chunk (all of the block's
+// 64-column panels at once) plus the block's Bt by one bulk copy; the MMA
+// warp computes D = V . Bt (hi and lo halves of V) into TMEM buffer
+// (item & 1); the two epilogue groups take alternate items, so two blocks
+// are in their TMEM -> registers -> shared -> TMA-store pipeline at once.
+//
+// warps: 0 TMA producer, 1 UMMA issuer, 2-3 P rows -> bf16 hi/lo V,
+//        4-7 epilogue group 0 (even items), 8-11 group 1 (odd items)
+template <int R, int NS, int EPI>
 __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
-    using L = ExpandLayout<R, NS>;
+    using L = ExpandLayout<R, NS, EPI>;
     extern __shared__ unsigned char sm_raw[];
     __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
     __shared__ __align__(8) uint64_t v_full[2], v_empty[2], d_full[2], d_empty[2];
     __shared__ uint32_t tslot;
+    __shared__ int s_u[2];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t raw = tc::smem_u32(sm_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -469,13 +682,14 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     if (tid == 32) {
         for (int i = 0; i < L::STAGES; ++i) {
             tc::mbar_init(&full[i], 1);
-            tc::mbar_init(&empty[i], 1 + 8);  // MMA commit (Bt read) + 8 epilogue warps (y stored)
+            // MMA commit (Bt read) [+ the item's 4 epilogue warps (y rows stored)]
+            tc::mbar_init(&empty[i], EPI == kEpiRmw ? 1 + 4 : 1);
         }
         for (int b = 0; b < 2; ++b) {
             tc::mbar_init(&v_full[b], 2);
             tc::mbar_init(&v_empty[b], 1);
             tc::mbar_init(&d_full[b], 1);
-            tc::mbar_init(&d_empty[b], 8);
+            tc::mbar_init(&d_empty[b], 4);
         }
         tc::fence_mbar_init();
     }
@@ -484,117 +698,106 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     tc::fence_after_sync();
     const uint32_t tmem = tslot;
     tc::pdl_launch_dependents();
-    tc::pdl_wait();  // everything below reads the previous kernels' output
-    ExpandItems it;
-    it.init(a, NS);
+    Blocks bl;
+    expand_blocks(bl, a, NS);
+    CostModel cm;
+    cm.units = a.units;
+    cm.load(a.counters);
+    cm.alpha = kSpChunk * 4;  // y read + write per column per chunk
+    cm.beta = 2 * R + 16;     // Bt bytes per column + per-item overhead
+    cm.G = gridDim.x;
+    int k0, k1;
+    item_range(cm, bl, s_u, k0, k1);  // K1's output only: before the wait (see the shrink)
+    const int nc = bl.nc;
+    tc::pdl_wait();  // P and y come from the previous kernels
+    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1792 + 2 * blockIdx.x] = tc::globaltimer();
 
     if (warp == 0) {
-        // producer: lane 4*pp + q issues y panel pp of chunk q, lane 16 the Bt chunk
+        // producer: lane q issues chunk q's 3D box, lane 16 the Bt block
         const uint64_t stream = tc::policy_evict_first();
-        const int pp = lane >> 2, q = lane & 3;
-        int stage = 0, npc = 0;
+        int stage = 0, npc = 0, pu = -1, row = 0, nch = 0, slot = 0;
         uint32_t phase = 0;
-        for (int w = it.w0; w < it.w1; ++w) {
-            const int4 U = a.units[w / it.ipu];
-            if (U.x >= a.slot_base) continue;
-            const int nch = U.z;
-            const int row = q < nch ? a.chunks[U.y + q].x : 0;
-            const int row0 = a.chunks[U.y].x;
-            const bool contig = unit_contiguous(a.chunks, U);
-            const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
-            for (int c = c0; c < c1; ++c) {
-                int s, j;
-                it.site_of(c, NS, s, j);
-                const int cw = it.cw[s];
-                const uint32_t bt_bytes = static_cast<uint32_t>(cw * R * 2);
-                if (lane == 0) {
-                    tc::mbar_wait(&empty[stage], phase ^ 1u);
-                    if (a.prof && blockIdx.x == 0 && npc < 128) a.prof[512 + npc * 4 + 0] = clock64();
-                    tc::mbar_expect_tx(&full[stage], static_cast<uint32_t>((cw / 64) * nch * kSpChunk * 128) + bt_bytes);
-                }
-                ++npc;
-                __syncwarp();
-                const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
-                if (contig) {
-                    if (lane < cw / 64)  // one 64-row box per panel
-                        tc::tma_load_2d_hint(st + lane * kSpU * 128, &maps.y64[s], j * cw + lane * 64, row0, &full[stage],
-                                             stream);
-                } else if (lane < 16 && pp < cw / 64 && q < nch) {
-                    tc::tma_load_2d_hint(st + pp * kSpU * 128 + q * (kSpChunk * 128), &maps.y[s], j * cw + pp * 64, row,
-                                         &full[stage], stream);
-                }
-                if (lane == 16)
-                    tc::bulk_load_1d(st + L::Y_BYTES,
-                                     static_cast<const unsigned char*>(a.site[s].Bt_tc) +
-                                         static_cast<long long>(U.x) * a.site[s].n * R * 2 +
-                                         static_cast<long long>(j) * bt_bytes,
-                                     bt_bytes, &full[stage]);
-                if (++stage == L::STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
+        for (int k = k0; k < k1; ++k) {
+            const int u = k / nc, c = k - u * nc;
+            if (u != pu) {
+                const int4 U = a.units[u];
+                nch = U.z;
+                slot = U.x;
+                row = lane < nch ? a.chunks[U.y + lane].x : 0;
+                pu = u;
+            }
+            const int s = bl.site(c), j = c - bl.first[s], cw = bl.cw[s];
+            const uint32_t bt_bytes = static_cast<uint32_t>(cw * R * 2);
+            if (lane == 0) {
+                tc::mbar_wait(&empty[stage], phase ^ 1u);
+                if (a.prof && blockIdx.x == 0 && npc < 128) a.prof[512 + npc * 4 + 0] = clock64();
+                tc::mbar_expect_tx(&full[stage], (EPI == kEpiRmw ? static_cast<uint32_t>(nch * (cw / 64) * kSpChunk * 128) : 0u) +
+                                                     bt_bytes);
+            }
+            ++npc;
+            __syncwarp();
+            const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
+            if (EPI == kEpiRmw && lane < nch)
+                tc::tma_load_3d_hint(st + lane * L::QS, &maps.y[s], 0, row, j * (cw / 64), &full[stage], stream);
+            if (lane == 16)
+                tc::bulk_load_1d(st + L::Y_BYTES,
+                                 static_cast<const unsigned char*>(a.site[s].Bt_tc) +
+                                     static_cast<long long>(slot) * a.site[s].n * R * 2 +
+                                     static_cast<long long>(j) * bt_bytes,
+                                 bt_bytes, &full[stage]);
+            if (++stage == L::STAGES) {
+                stage = 0;
+                phase ^= 1u;
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             const uint32_t id128 = tc::idesc_bf16_f32(kSpU, kSpN), id256 = tc::idesc_bf16_f32(kSpU, kSpNMax);
-            int stage = 0, visit = 0, dc = 0, prev = -1;
+            int stage = 0, visit = 0;
             uint32_t phase = 0;
-            for (int w = it.w0; w < it.w1; ++w) {
-                const int u = w / it.ipu;
-                const int4 U = a.units[u];
-                if (U.x >= a.slot_base) continue;
+            for (int k = k0; k < k1; ++k) {
+                const int u = k / nc, c = k - u * nc, jt = k - k0;
                 const int vb = visit & 1;
-                if (u != prev) {
+                if (k == k0 || c == 0) {
                     tc::mbar_wait(&v_full[vb], (visit >> 1) & 1);
                     tc::fence_after_sync();
-                    prev = u;
                 }
-                const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
-                for (int c = c0; c < c1; ++c) {
-                    int s, j;
-                    it.site_of(c, NS, s, j);
-                    const uint32_t vhi = sbase + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES, vlo = vhi + L::V_BYTES;
-                    tc::mbar_wait(&full[stage], phase);
-                    const int db = dc & 1;
-                    tc::mbar_wait(&d_empty[db], ((dc >> 1) & 1) ^ 1u);
-                    tc::fence_after_sync();
-                    if (a.prof && blockIdx.x == 0 && dc < 128) a.prof[512 + dc * 4 + 1] = clock64();
-                    const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
-                    const uint32_t dD = tmem + db * kSpNMax;
-                    const uint32_t id = it.cw[s] == kSpNMax ? id256 : id128;
+                const int s = bl.site(c);
+                const uint32_t vhi = sbase + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES, vlo = vhi + L::V_BYTES;
+                tc::mbar_wait(&full[stage], phase);
+                const int db = jt & 1;
+                tc::mbar_wait(&d_empty[db], ((jt >> 1) & 1) ^ 1u);
+                tc::fence_after_sync();
+                if (a.prof && blockIdx.x == 0 && jt < 128) a.prof[512 + jt * 4 + 1] = clock64();
+                const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
+                const uint32_t dD = tmem + db * kSpNMax;
+                const uint32_t id = bl.cw[s] == kSpNMax ? id256 : id128;
 #pragma unroll
-                    for (int k = 0; k < R / 16; ++k) {
-                        const uint64_t bd = tc::desc_kmajor(bt + k * 256, 128, R * 16);
-                        tc::mma_bf16(dD, tc::desc_kmajor(vhi + k * 256, 128, R * 16), bd, id, k > 0 ? 1u : 0u);
-                        tc::mma_bf16(dD, tc::desc_kmajor(vlo + k * 256, 128, R * 16), bd, id, 1u);
-                    }
-                    tc::mma_commit(&d_full[db]);
-                    tc::mma_commit(&empty[stage]);
-                    if (++stage == L::STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                    ++dc;
+                for (int kk = 0; kk < R / 16; ++kk) {
+                    const uint64_t bd = tc::desc_kmajor(bt + kk * 256, 128, R * 16);
+                    tc::mma_bf16(dD, tc::desc_kmajor(vhi + kk * 256, 128, R * 16), bd, id, kk > 0 ? 1u : 0u);
+                    tc::mma_bf16(dD, tc::desc_kmajor(vlo + kk * 256, 128, R * 16), bd, id, 1u);
+                }
+                tc::mma_commit(&d_full[db]);
+                tc::mma_commit(&empty[stage]);
+                if (++stage == L::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
                 // the unit's V buffer is free once its last item has been issued
-                const bool last = w + 1 >= it.w1 || (w + 1) / it.ipu != u;
-                if (last) {
+                if (k + 1 == k1 || c + 1 == nc) {
                     tc::mma_commit(&v_empty[vb]);
                     ++visit;
-                    prev = -1;
                 }
             }
         }
     } else if (warp < 4) {
         // P rows -> V = scale * P (bf16 hi + lo), 32 rows per warp, once per unit visit
-        int visit = 0, prev = -1;
-        for (int w = it.w0; w < it.w1; ++w) {
-            const int u = w / it.ipu;
+        int visit = 0;
+        for (int k = k0; k < k1; ++k) {
+            const int u = k / nc;
+            if (!(k == k0 || k == u * nc)) continue;
             const int4 U = a.units[u];
-            if (U.x >= a.slot_base) continue;
-            if (u == prev) continue;
-            prev = u;
             const int vb = visit & 1;
             const int m = (warp - 2) * 32 + lane, q = m >> 4, rr = m & 15;
             const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
@@ -606,11 +809,11 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                 const float sc = __ldg(static_cast<const float*>(a.site[s].scale) + U.x);
                 unsigned char* vhi = sgen + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES;
 #pragma unroll
-                for (int k0 = 0; k0 < R; k0 += 8) {
+                for (int k0v = 0; k0v < R; k0v += 8) {
                     float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
                     if (valid) {
-                        p0 = *reinterpret_cast<const float4*>(pr + s * R + k0);
-                        p1 = *reinterpret_cast<const float4*>(pr + s * R + k0 + 4);
+                        p0 = *reinterpret_cast<const float4*>(pr + s * R + k0v);
+                        p1 = *reinterpret_cast<const float4*>(pr + s * R + k0v + 4);
                     }
                     const float v[8] = {p0.x * sc, p0.y * sc, p0.z * sc, p0.w * sc,
                                         p1.x * sc, p1.y * sc, p1.z * sc, p1.w * sc};
@@ -622,7 +825,7 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
                         bf16x2_to_acc(hi[e], h0, h1);
                         lo[e] = f32x2_to_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
                     }
-                    const uint32_t off = tc::kmajor_offset(m, k0, R);
+                    const uint32_t off = tc::kmajor_offset(m, k0v, R);
                     *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                     *reinterpret_cast<uint4*>(vhi + L::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
                 }
@@ -633,53 +836,94 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
             ++visit;
         }
     } else {
-        // epilogue: D -> registers, y chunk += D in shared memory, TMA store
-        const int q = warp & 3, hf = (warp - 4) >> 2;
+        // epilogue group g takes items k0 + g, k0 + g + 2, ...: D -> registers,
+        // y block += D in shared memory, TMA store (one 3D box per full chunk)
+        const int q = warp & 3, g = (warp - 4) >> 2;
         const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
         const uint64_t stream = tc::policy_evict_first();
         const int r1 = lane >> 2, cp = 2 * (lane & 3);
-        int stage = 0, dc = 0, pend = -1;
-        uint32_t phase = 0;
-        for (int w = it.w0; w < it.w1; ++w) {
-            const int4 U = a.units[w / it.ipu];
-            if (U.x >= a.slot_base) continue;
-            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-            const int c0 = (w % it.ipu) * kExpBlock, c1 = min(it.nc, c0 + kExpBlock);
-            for (int c = c0; c < c1; ++c) {
-                int s, j;
-                it.site_of(c, NS, s, j);
-                const int cw = it.cw[s], npw = cw / 128;  // 64-column panels per warp: 1 or 2
-                const int db = dc & 1;
-                tc::mbar_wait(&d_full[db], (dc >> 1) & 1);
-                tc::mbar_wait(&full[stage], phase);
-                tc::fence_after_sync();
-                if (a.prof && blockIdx.x == 0 && warp == 4 && lane == 0 && dc < 128) a.prof[512 + dc * 4 + 2] = clock64();
-                uint32_t v[2][32];
-                // both loads unconditionally, then the wait: a tcgen05.ld whose
-                // issue sits under a branch lets the compiler merge its output
-                // registers at the join BEFORE tcgen05.wait::ld, i.e. copy
-                // registers the load has not written yet (found as stale D
-                // columns 120-127 of 256-wide chunks).  For 128-wide chunks the
-                // second load reads the other half's columns and is ignored.
-                tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpNMax + hf * (cw / 2), v[0]);
-                tc::tmem_ld_16x256b_x8(tmem + lane_base + db * kSpNMax + hf * (cw / 2) + 64, v[1]);
-                tc::tmem_ld_wait();
+        int pu = -1;
+        int2 ch = make_int2(0, 0);
+        for (int k = k0 + g; k < k1; k += 2) {
+            const int u = k / nc, c = k - u * nc, jt = k - k0;
+            if (u != pu) {
+                const int4 U = a.units[u];
+                ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
+                pu = u;
+            }
+            const int s = bl.site(c), j = c - bl.first[s], cw = bl.cw[s], npan = cw / 64;
+            const int stage = jt % L::STAGES;
+            const uint32_t phase = static_cast<uint32_t>(jt / L::STAGES) & 1u;
+            tc::mbar_wait(&d_full[g], (jt >> 1) & 1);
+            if (EPI == kEpiRmw) tc::mbar_wait(&full[stage], phase);
+            tc::fence_after_sync();
+            if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128)
+                a.prof[512 + jt * 4 + 2] = clock64();
+            if constexpr (EPI == kEpiReduce) {
+                // staging buffer (group g, item parity), this chunk's [panel][16][128 B]
+                const int sb = (jt >> 1) & 1;
+                const uint32_t tile = L::OFF_STG + ((g * 2 + sb) * 4 + q) * L::QS;
+                if (lane == 0) tc::tma_store_wait_read_1();  // this buffer's reduce of 2 items ago has read it
+                __syncwarp();
+                if (ch.y > 0) {
+                    for (int pass = 0; pass < npan / 2; ++pass) {
+                        uint32_t v[2][32];
+                        tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128, v[0]);
+                        tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128 + 64, v[1]);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (int pw = 0; pw < 2; ++pw) {
+                            const uint32_t panel = tile + (2 * pass + pw) * (kSpChunk * 128);
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                                for (int half = 0; half < 2; ++half) {
+                                    const int r = r1 + 8 * half;
+                                    const uint32_t w = r < ch.y ? f32x2_to_bf16(__uint_as_float(v[pw][4 * i + 2 * half]),
+                                                                                 __uint_as_float(v[pw][4 * i + 2 * half + 1]))
+                                                                : 0x80008000u;  // -0.0: y + (-0) == y bit for bit
+                                    *reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(r, 8 * i + cp, kSpChunk)) = w;
+                                }
+                        }
+                    }
+                }
                 tc::fence_before_sync();
                 __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&d_empty[db]);
+                if (lane == 0) tc::mbar_arrive(&d_empty[g]);
                 if (ch.y > 0) {
+                    tc::fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) tc::tma_reduce_add_3d(&maps.y[s], 0, ch.x, j * npan, sbase + tile);
+                }
+                if (lane == 0) {
+                    tc::tma_store_commit();
+                    if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && jt < 128) a.prof[512 + jt * 4 + 3] = clock64();
+                }
+                __syncwarp();
+                continue;
+            }
+            const uint32_t tile = L::OFF_RING + stage * L::STAGE + q * L::QS;  // this chunk's [panel][16][128 B]
+            if (ch.y > 0) {
+                for (int pass = 0; pass < npan / 2; ++pass) {
+                    uint32_t v[2][32];
+                    // loads, wait and every use of v stay in one block: a
+                    // tcgen05.ld whose registers are live across a branch join
+                    // can have them copied before tcgen05.wait::ld (stale D)
+                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128, v[0]);
+                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128 + 64, v[1]);
+                    tc::tmem_ld_wait();
+                    if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128 && pass == 0)
+                        a.prof[1024 + jt * 4 + 2] = clock64();
 #pragma unroll
                     for (int pw = 0; pw < 2; ++pw) {
-                        if (pw >= npw) break;
-                        const int pan = hf * npw + pw;  // 64-column panel of the chunk
-                        const uint32_t panel = L::OFF_RING + stage * L::STAGE + pan * kSpU * 128;
+                        const uint32_t panel = tile + (2 * pass + pw) * (kSpChunk * 128);
                         uint32_t hv[16];
 #pragma unroll
                         for (int i = 0; i < 8; ++i)
 #pragma unroll
                             for (int half = 0; half < 2; ++half)
                                 hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
-                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64));
+                                    sgen + panel + tc::sw128_offset(r1 + 8 * half, 8 * i + cp, kSpChunk));
 #pragma unroll
                         for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -695,60 +939,63 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
 #pragma unroll
                             for (int half = 0; half < 2; ++half)
                                 *reinterpret_cast<uint32_t*>(
-                                    sgen + panel + tc::sw128_offset(q * kSpChunk + r1 + 8 * half, 8 * i + cp, 64)) =
+                                    sgen + panel + tc::sw128_offset(r1 + 8 * half, 8 * i + cp, kSpChunk)) =
                                     hv[2 * i + half];
                     }
-                    tc::fence_proxy_async();
-                    __syncwarp();
-                    for (int pw = 0; pw < npw; ++pw) {
-                        const int pan = hf * npw + pw;
-                        const uint32_t panel = L::OFF_RING + stage * L::STAGE + pan * kSpU * 128;
-                        if (ch.y == kSpChunk) {
-                            if (lane == 0)
-                                tc::tma_store_2d_hint(&maps.y[s], j * cw + pan * 64, ch.x,
-                                                      sbase + panel + q * (kSpChunk * 128), stream);
-                        } else {
-                            __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y);
-                            for (int idx = lane; idx < ch.y * 8; idx += 32) {
-                                const int rr = idx >> 3, c16 = idx & 7;
-                                const uint4 val = *reinterpret_cast<const uint4*>(
-                                    sgen + panel + tc::sw128_offset(q * kSpChunk + rr, c16 * 8, 64));
-                                *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * a.site[s].ldy +
-                                                          j * cw + pan * 64 + c16 * 8) = val;
-                            }
-                        }
-                    }
                 }
-                if (lane == 0) {
-                    // release the PREVIOUS stage once its store has read shared
-                    // memory: the store of this chunk drains while the next is processed
-                    tc::tma_store_commit();
-                    tc::tma_store_wait_read_1();
-                    if (pend >= 0) tc::mbar_arrive(&empty[pend]);
-                    pend = stage;
-                    if (a.prof && blockIdx.x == 0 && warp == 4 && dc < 128) a.prof[512 + dc * 4 + 3] = clock64();
-                }
-                __syncwarp();
-                if (++stage == L::STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-                ++dc;
             }
+            if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128)
+                a.prof[1024 + jt * 4 + 0] = clock64();
+            // D is free once read (warps without rows read nothing)
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&d_empty[g]);
+            if (ch.y > 0 && (a.flags & kSplitTmaStore)) {
+                tc::fence_proxy_async();
+                __syncwarp();
+                if (ch.y == kSpChunk && lane == 0) tc::tma_store_3d_hint(&maps.y[s], 0, ch.x, j * npan, sbase + tile, stream);
+            }
+            if (ch.y > 0 && (ch.y < kSpChunk || !(a.flags & kSplitTmaStore))) {
+                // rows straight from shared memory to global: 16 B per lane, a
+                // row's 256 or 128 columns per 32 or 16 lanes (coalesced), and
+                // only the chunk's own rows (past ch.y belong to other entries);
+                // the TMA engine then carries only the loads
+                __syncwarp();
+                __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y) + j * cw;
+                const long long ldy = a.site[s].ldy;
+                const int lg = cw == kSpNMax ? 5 : 4;  // log2(16 B vectors per row)
+                for (int idx = lane; idx < (ch.y << lg); idx += 32) {
+                    const int rr = idx >> lg, v16 = idx & ((1 << lg) - 1), pan = v16 >> 3, c16 = v16 & 7;
+                    const uint4 val = *reinterpret_cast<const uint4*>(
+                        sgen + tile + pan * (kSpChunk * 128) + tc::sw128_offset(rr, c16 * 8, kSpChunk));
+                    *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * ldy + pan * 64 + c16 * 8) = val;
+                }
+            }
+            if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128)
+                a.prof[1024 + jt * 4 + 1] = clock64();
+            __syncwarp();
+            if (lane == 0) {
+                // the stage is free once this item's stores have read shared
+                // memory (st.global: issued = read; TMA: wait for its reads)
+                if (a.flags & kSplitTmaStore) {
+                    tc::tma_store_commit();
+                    tc::tma_store_wait_read();
+                }
+                tc::mbar_arrive(&empty[stage]);
+                if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && jt < 128) a.prof[512 + jt * 4 + 3] = clock64();
+            }
+            __syncwarp();
         }
-        if (lane == 0) {
-            tc::tma_store_wait_all();
-            if (pend >= 0) tc::mbar_arrive(&empty[pend]);
-        }
+        if (lane == 0) tc::tma_store_wait_all();
     }
     tc::fence_before_sync();
     __syncthreads();
+    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1793 + 2 * blockIdx.x] = tc::globaltimer();
     if (warp == 0) {
         __syncwarp();
         tc::tmem_dealloc(tmem, 512);
     }
 }
-
 // ---------------------------------------------------------------- dispatch
 
 using SplitFn = void (*)(SplitArgs);
@@ -825,6 +1072,18 @@ static int fill_common(SplitArgs& args, const preft_meta_t* meta, const preft_lo
     return PREFT_OK;
 }
 
+template <int EPI>
+static int launch_expand(const SplitMaps& maps, const SplitArgs& args, int nsites, int r, int num_sms, cudaStream_t stream) {
+    if (r == 16) {
+        if (nsites == 1) return launch_tc(expand_tc_kernel<16, 1, EPI>, ExpandLayout<16, 1, EPI>::SMEM, 384, maps, args, num_sms, stream);
+        if (nsites == 2) return launch_tc(expand_tc_kernel<16, 2, EPI>, ExpandLayout<16, 2, EPI>::SMEM, 384, maps, args, num_sms, stream);
+        return launch_tc(expand_tc_kernel<16, 3, EPI>, ExpandLayout<16, 3, EPI>::SMEM, 384, maps, args, num_sms, stream);
+    }
+    if (nsites == 1) return launch_tc(expand_tc_kernel<32, 1, EPI>, ExpandLayout<32, 1, EPI>::SMEM, 384, maps, args, num_sms, stream);
+    if (nsites == 2) return launch_tc(expand_tc_kernel<32, 2, EPI>, ExpandLayout<32, 2, EPI>::SMEM, 384, maps, args, num_sms, stream);
+    return PREFT_ERR_RANK;
+}
+
 static long long* g_split_prof = nullptr;
 void split_set_profile(long long* buf) { g_split_prof = buf; }
 
@@ -840,6 +1099,35 @@ int split_variant() {
     return g_split_variant;
 }
 void set_split_variant(int v) { g_split_variant = v; }
+
+// Floats of meta->lora_part the tensor-core split uses: kPlanes planes of
+// [T_cap][64] f32 (plane 0 is P itself on the preft_lora_apply route) and
+// one int per unit (the shrink's per-unit arrival counters, kept zero
+// between launches).
+long long lora_part_floats_needed(const preft_meta_t* meta) {
+    return static_cast<long long>(kPlanes) * meta->T_cap * 64 + meta->chunk_cap;
+}
+
+// the shrink's partial planes (p >= 1) and arrival counters, from the meta's
+// workspace; one plane (whole units per CTA) without it
+static void split_planes(SplitArgs& args, const preft_meta_t* meta) {
+    args.max_planes = 1;
+    args.planes = nullptr;
+    args.plane_stride = 0;
+    args.sync = nullptr;
+    // default one plane (whole units per CTA): at config-4 shapes the K-split
+    // schedule balances the CTAs (busy max/mean 1.3 -> 1.1) but its
+    // per-visit fixup (fence + atomic + plane sum) costs more than it saves
+    // (cfg4 12.0 ms/step with whole units vs 14.2 with 4 planes, r02i)
+    const char* env = getenv("PREFT_SPLIT_PLANES");
+    const int want = env ? atoi(env) : 1;
+    if (meta->lora_part && meta->lora_part_floats >= lora_part_floats_needed(meta) && want > 1) {
+        args.max_planes = want < kPlanes ? want : kPlanes;
+        args.planes = meta->lora_part;
+        args.plane_stride = static_cast<long long>(meta->T_cap) * 64;
+        args.sync = reinterpret_cast<int*>(meta->lora_part + static_cast<long long>(kPlanes) * meta->T_cap * 64);
+    }
+}
 
 // Can the tcgen05 pair (shrink + expand) run this group?  Shared by the split
 // entry points and by lora_apply's r >= 16 route.
@@ -898,14 +1186,8 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
             if (!make_tmap_bf16_sw128(&maps.A[s], sites[s].A, 1ull << 20, static_cast<unsigned long long>(m),
                                       static_cast<unsigned long long>(m), 64, static_cast<unsigned>(r)))
                 return PREFT_ERR_CONFIG;
-        // two K halves per unit when the unit's K range is long enough to split
-        // (P must start at zero: the halves accumulate into it)
-        args.ks = getenv("PREFT_SPLIT_KS") ? atoi(getenv("PREFT_SPLIT_KS")) : 1;
+        split_planes(args, meta);
         args.prof = g_split_prof;
-        if (args.ks > 1) {
-            const cudaError_t e = cudaMemsetAsync(P, 0, static_cast<size_t>(rows) * ldp * sizeof(float), stream);
-            if (e != cudaSuccess) return -static_cast<int>(e);
-        }
         if (r == 16) {
             if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
             if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
@@ -938,27 +1220,25 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
     SplitArgs args{};
     fill_common(args, meta, sites, nsites, const_cast<void*>(P), ldp);
     args.prof = g_split_prof;
+    {
+        const char* env = getenv("PREFT_SPLIT_TMA_STORE");
+        args.flags = (env && env[0] == '1') ? kSplitTmaStore : 0;
+    }
     const int variant = split_variant();
     const bool tc_ok = expand_tc_ok(meta, P, ldp, sites, nsites, r, dtype);
     if (variant == 1 && !tc_ok) return PREFT_ERR_SHAPE;
     if (variant != 0 && tc_ok) {
         SplitMaps maps{};
-        for (int s = 0; s < nsites; ++s)
-            if (!make_tmap_bf16_sw128(&maps.y[s], sites[s].y, static_cast<unsigned long long>(rows),
-                                      static_cast<unsigned long long>(sites[s].n),
-                                      static_cast<unsigned long long>(sites[s].ldy), 64, kSpChunk) ||
-                !make_tmap_bf16_sw128(&maps.y64[s], sites[s].y, static_cast<unsigned long long>(rows),
-                                      static_cast<unsigned long long>(sites[s].n),
-                                      static_cast<unsigned long long>(sites[s].ldy), 64, kSpU))
+        for (int s = 0; s < nsites; ++s) {
+            const unsigned npan = (sites[s].n % kSpNMax == 0 ? kSpNMax : kSpN) / 64;
+            if (!make_tmap_bf16_panels(&maps.y[s], sites[s].y, static_cast<unsigned long long>(rows),
+                                       static_cast<unsigned long long>(sites[s].n),
+                                       static_cast<unsigned long long>(sites[s].ldy), kSpChunk, npan))
                 return PREFT_ERR_CONFIG;
-        if (r == 16) {
-            if (nsites == 1) return launch_tc(expand_tc_kernel<16, 1>, ExpandLayout<16, 1>::SMEM, 384, maps, args, num_sms, stream);
-            if (nsites == 2) return launch_tc(expand_tc_kernel<16, 2>, ExpandLayout<16, 2>::SMEM, 384, maps, args, num_sms, stream);
-            return launch_tc(expand_tc_kernel<16, 3>, ExpandLayout<16, 3>::SMEM, 384, maps, args, num_sms, stream);
         }
-        if (nsites == 1) return launch_tc(expand_tc_kernel<32, 1>, ExpandLayout<32, 1>::SMEM, 384, maps, args, num_sms, stream);
-        if (nsites == 2) return launch_tc(expand_tc_kernel<32, 2>, ExpandLayout<32, 2>::SMEM, 384, maps, args, num_sms, stream);
-        return PREFT_ERR_RANK;
+        const char* epi = getenv("PREFT_SPLIT_EPI");
+        if (epi && epi[0] == 'r' && epi[1] == 'm') return launch_expand<kEpiRmw>(maps, args, nsites, r, num_sms, stream);
+        return launch_expand<kEpiReduce>(maps, args, nsites, r, num_sms, stream);
     }
     const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;
     bool vec = true;

@@ -79,6 +79,7 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
     __shared__ int s_warp[32];
     __shared__ int s_total;
     __shared__ int s_split;
+    __shared__ int s_lora_units, s_lora_chunks;
     __shared__ int s_err;
 
     const int tid = threadIdx.x;
@@ -261,6 +262,21 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
         }
         __syncthreads();
         nunits = block_scan_array(C, nseg, s_warp, &s_total);
+        // LoRA-class units (slot < slot_split) come first: their count is the
+        // unit offset of the first ReFT-class segment
+        if (tid == 0) {
+            s_lora_units = nunits;
+            s_lora_chunks = nchunks;
+        }
+        __syncthreads();
+        for (int s = tid; s < nseg; s += blockDim.x) {
+            const int sl = m.segments[3 * s + 0];
+            if (sl >= m.slot_split && (s == 0 || m.segments[3 * (s - 1) + 0] < m.slot_split)) {
+                s_lora_units = C[s];
+                s_lora_chunks = A[s];
+            }
+        }
+        __syncthreads();
         for (int j = tid; j < nunits; j += blockDim.x) {
             int lo = 0, hi = nseg - 1;  // last segment with C[s] <= j
             while (lo < hi) {
@@ -280,6 +296,8 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
     if (tid == 0) {
         m.counters[PREFT_CTR_CHUNKS] = chunks_fit ? nchunks : 0;
         m.counters[PREFT_CTR_UNITS] = nunits;
+        m.counters[PREFT_CTR_LORA_UNITS] = chunks_fit ? s_lora_units : 0;
+        m.counters[PREFT_CTR_LORA_CHUNKS] = chunks_fit ? s_lora_chunks : 0;
         m.counters[PREFT_CTR_SEL_TOKENS] = n_tok;
         m.counters[PREFT_CTR_SEGMENTS] = nseg;
         m.counters[PREFT_CTR_TILES] = ntiles;

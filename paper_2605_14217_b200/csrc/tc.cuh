@@ -197,6 +197,24 @@ __device__ __forceinline__ void tma_load_2d_hint(uint32_t sdst, const void* tmap
         : "memory");
 }
 
+// 3D tensor-map load / store (coordinates innermost first), L2 cache hint
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t sdst, const void* tmap, int c0, int c1, int c2,
+                                                 uint64_t* mbar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(sdst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(mbar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_3d_hint(const void* tmap, int c0, int c1, int c2, uint32_t ssrc,
+                                                  uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], [%4], %5;" ::
+            "l"(reinterpret_cast<uint64_t>(tmap)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(ssrc), "l"(policy)
+        : "memory");
+}
+
 // 2D tensor-map store with an L2 cache hint (bulk async group)
 __device__ __forceinline__ void tma_store_2d_hint(const void* tmap, int c0, int c1, uint32_t ssrc, uint64_t policy) {
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group.L2::cache_hint [%0, {%1, %2}], [%3], %4;" ::
@@ -211,6 +229,13 @@ __device__ __forceinline__ void tma_reduce_add_2d(const void* tmap, int c0, int 
     asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
                      reinterpret_cast<uint64_t>(tmap)),
                  "r"(c0), "r"(c1), "r"(ssrc)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_reduce_add_3d(const void* tmap, int c0, int c1, int c2, uint32_t ssrc) {
+    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::
+                     "l"(reinterpret_cast<uint64_t>(tmap)),
+                 "r"(c0), "r"(c1), "r"(c2), "r"(ssrc)
                  : "memory");
 }
 

@@ -148,11 +148,13 @@ class BatchMeta:
         return self.build_arrays(qsl, slots, flags, stream, slot_split=slot_split)
 
     def ensure_lora_part(self) -> None:
-        """Attach the f32 workspace [T_cap][<= 64] the tensor-core LoRA route
-        keeps the rank-r intermediate in (allocated once, fixed address, so
-        plans and captured graphs stay valid)."""
+        """Attach the zeroed f32 workspace of the tensor-core LoRA split: the
+        rank-r intermediate P [T_cap][<= 64] and the shrink's partial planes
+        and per-unit arrival counters (preft_lora_part_floats; allocated once,
+        fixed address, so plans and captured graphs stay valid)."""
         if self.lora_part is None:
-            self.lora_part = torch.zeros(self.T_cap * 64, dtype=torch.float32, device=self.device)
+            n = int(_lib.load().preft_lora_part_floats(ctypes.byref(self.c)))
+            self.lora_part = torch.zeros(max(n, self.T_cap * 64), dtype=torch.float32, device=self.device)
             self.c.lora_part = self.lora_part.data_ptr()
             self.c.lora_part_floats = self.lora_part.numel()
 

@@ -123,6 +123,8 @@ class SplitWorkspace:
 
         self.T_cap = meta.T_cap
         self.P = torch.empty(meta.T_cap * 3 * pool.lora_rank, dtype=pool.acc, device=pool.device)
+        # the tensor-core shrink's partial planes and arrival counters
+        meta.ensure_lora_part()
 
     def view(self, T: int, width: int):
         """Contiguous [T][width] view (the all-reduce moves exactly these bytes)."""

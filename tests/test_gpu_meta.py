@@ -36,6 +36,13 @@ def _check_meta(meta, qsl, slots, flags, tile_tokens, split):
     assert c[_lib.CTR_CHUNKS] == len(chunks) and c[_lib.CTR_UNITS] == len(units)
     assert np.array_equal(meta.chunks_host(), chunks)
     assert np.array_equal(meta.units_host(), units)
+    # LoRA-class units (slot < split) lead the unit list; their count
+    u_slot = np.asarray(units).reshape(-1, 4)[:, 0]
+    n_lora = int(c[_lib.CTR_LORA_UNITS])
+    assert n_lora == int(np.sum(u_slot < split))
+    assert (u_slot[:n_lora] < split).all() and (u_slot[n_lora:] >= split).all()
+    u_nch = np.asarray(units).reshape(-1, 4)[:, 2]
+    assert int(c[_lib.CTR_LORA_CHUNKS]) == int(u_nch[:n_lora].sum())
 
 
 def test_masks_and_grouping_on_golden_batches(cuda_device):
