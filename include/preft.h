@@ -229,6 +229,60 @@ int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int6
  * partial planes of P for units the shrink shares between CTAs, plus one
  * arrival counter per unit.  With less, every unit's shrink stays on one CTA. */
 int64_t preft_lora_part_floats(const preft_meta_t* meta);
+/*
+ * Fused tensor-parallel LoRA^P: shrink -> cross-rank exchange of the rank-r
+ * partials -> expand in ONE persistent tcgen05 kernel (replaces the
+ * preft_lora_shrink + NCCL all-reduce + preft_lora_expand sequence above for
+ * the same model.py:449-451 / adapters.py:284-288 delta).
+ *
+ * Every rank owns one exchange region (preft_xchg_region_bytes, zeroed once)
+ * that its peers can address (cudaIpc / the same device when tp_size == 1):
+ *   part [2 parities][tp src][planes][T_cap][64] f32 — src's partial P rows
+ *   flag [2 parities][tp src][planes][U_cap] int32 — tag of the launch that
+ *                                                      wrote them
+ *   state [4] int32 — launch count, finished CTAs, error bits
+ * A CTA that finishes a unit's shrink piece stores its partial rows into
+ * every rank's region (P2P stores over NVLink) and then the piece's flag
+ * (system-scope release); the expand of that unit waits for all tp x pieces
+ * flags of the launch and sums the partials in (src, piece) order, so every
+ * rank computes the same V bit for bit.  Consecutive launches alternate
+ * parities (the device-side launch count), which is what lets a fast rank
+ * start the next launch while a slow one still reads this one.  All ranks
+ * must issue the same sequence of fused launches on their exchanges.
+ * A wait that exceeds spin_ns (default 2 s) sets state[2] bit 0 and gives up
+ * (the output is then wrong; preft_xchg_errors reads the bits).
+ */
+#define PREFT_XCHG_MAX_TP 8
+typedef struct preft_xchg {
+    int32_t tp_size;
+    int32_t tp_rank;
+    int32_t planes;    /* K-split pieces per unit and rank, 1..4 */
+    int32_t T_cap;     /* rows of every partial plane (>= meta->T_cap) */
+    int32_t U_cap;     /* units (>= meta->chunk_cap) */
+    int32_t peer_sys;  /* 1: the peers are other devices (system-scope ordering) */
+    int32_t grid;      /* CTAs per launch, 0 = the SM count; must match on every rank */
+    int32_t reserved;
+    float* part[PREFT_XCHG_MAX_TP];    /* part[d]: rank d's partial planes, as mapped here */
+    int32_t* flag[PREFT_XCHG_MAX_TP];  /* flag[d]: rank d's flags */
+    int32_t* state;                    /* this rank's state words */
+    int64_t spin_ns;
+} preft_xchg_t;
+int64_t preft_xchg_region_bytes(int32_t tp_size, int32_t planes, int32_t T_cap, int32_t U_cap);
+/* fill part/flag/state from the base address of every rank's region */
+int preft_xchg_init(preft_xchg_t* xg, void* const* region_bases, int32_t tp_size, int32_t tp_rank,
+                    int32_t planes, int32_t T_cap, int32_t U_cap, int32_t peer_sys);
+int preft_lora_fused(const preft_meta_t* meta, const void* x, int64_t rows, int64_t ldx, int32_t m,
+                     const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype,
+                     const preft_xchg_t* xchg, void* stream);
+/* state[2] of this rank's region (stream-ordered read; synchronises the stream) */
+int preft_xchg_errors(const preft_xchg_t* xchg, void* stream, int32_t* out);
+/* cudaIpc plumbing for the exchange regions of a multi-GPU TP group:
+ * a zeroed device allocation, its 64-byte IPC handle, and the peer mapping */
+int preft_dev_alloc(int64_t bytes, void** out);
+int preft_dev_free(void* p);
+int preft_ipc_handle(void* dev_ptr, void* handle_out /* 64 bytes */);
+int preft_ipc_open(const void* handle /* 64 bytes */, void** dev_ptr_out);
+int preft_ipc_close(void* dev_ptr);
 /* split-kernel variant: -1 automatic, 0 SIMT only, 1 tensor cores only
  * (PREFT_ERR_SHAPE when ineligible).  Env: PREFT_SPLIT_VARIANT=simt|tc. */
 int preft_set_split_variant(int32_t variant);

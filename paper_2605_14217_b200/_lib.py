@@ -74,6 +74,28 @@ class PreftMeta(ctypes.Structure):
     ]
 
 
+XCHG_MAX_TP = 8
+
+
+class PreftXchg(ctypes.Structure):
+    """preft_xchg_t: one rank's view of the fused kernel's exchange regions."""
+
+    _fields_ = [
+        ("tp_size", ctypes.c_int32),
+        ("tp_rank", ctypes.c_int32),
+        ("planes", ctypes.c_int32),
+        ("T_cap", ctypes.c_int32),
+        ("U_cap", ctypes.c_int32),
+        ("peer_sys", ctypes.c_int32),
+        ("grid", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("part", ctypes.c_void_p * XCHG_MAX_TP),
+        ("flag", ctypes.c_void_p * XCHG_MAX_TP),
+        ("state", ctypes.c_void_p),
+        ("spin_ns", ctypes.c_int64),
+    ]
+
+
 class PreftLoraSite(ctypes.Structure):
     _fields_ = [
         ("A", ctypes.c_void_p),
@@ -157,6 +179,34 @@ SIGNATURES = {
             ctypes.c_void_p,
         ],
     ),
+    "preft_xchg_region_bytes": (ctypes.c_int64, [ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32]),
+    "preft_xchg_init": (
+        ctypes.c_int,
+        [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p), ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+         ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
+    ),
+    "preft_lora_fused": (
+        ctypes.c_int,
+        [
+            ctypes.POINTER(PreftMeta),
+            ctypes.c_void_p,
+            ctypes.c_int64,
+            ctypes.c_int64,
+            ctypes.c_int32,
+            ctypes.POINTER(PreftLoraSite),
+            ctypes.c_int32,
+            ctypes.c_int32,
+            ctypes.c_int32,
+            ctypes.c_void_p,
+            ctypes.c_void_p,
+        ],
+    ),
+    "preft_xchg_errors": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p, ctypes.POINTER(ctypes.c_int32)]),
+    "preft_dev_alloc": (ctypes.c_int, [ctypes.c_int64, ctypes.POINTER(ctypes.c_void_p)]),
+    "preft_dev_free": (ctypes.c_int, [ctypes.c_void_p]),
+    "preft_ipc_handle": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "preft_ipc_open": (ctypes.c_int, [ctypes.c_void_p, ctypes.POINTER(ctypes.c_void_p)]),
+    "preft_ipc_close": (ctypes.c_int, [ctypes.c_void_p]),
     "preft_set_split_variant": (ctypes.c_int, [ctypes.c_int32]),
     "preft_diag_split": (ctypes.c_int, [ctypes.c_void_p]),
     "preft_lora_part_floats": (ctypes.c_int64, [ctypes.POINTER(PreftMeta)]),

@@ -1,6 +1,7 @@
 // extern "C" surface of libpreft (declared in include/preft.h) and K4, the
 // f64 -> pool-slab conversion used by adapter registration / weight sync.
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -24,6 +25,12 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
 int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long long rows, const preft_lora_site_t* sites,
                 int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
 int reft_tc_last_grid();
+long long xchg_region_bytes(int tp, int planes, int T_cap, int U_cap);
+int xchg_init(preft_xchg_t* xg, void* const* bases, int tp, int rank, int planes, int T_cap, int U_cap, int peer_sys);
+int lora_fused(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
+               const preft_lora_site_t* sites, int nsites, int r, int dtype, const preft_xchg_t* xg,
+               cudaStream_t stream, int num_sms);
+int xchg_errors(const preft_xchg_t* xg, cudaStream_t stream, int* out);
 void reft_tc_set_profile(long long* buf);
 void reft_tc_set_flags(int flags, int look);
 
@@ -195,6 +202,64 @@ int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int6
                       const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype, void* stream) {
     return finish(lora_expand(meta, P, ldp, rows, sites, nsites, r_max, dtype, static_cast<cudaStream_t>(stream),
                               current_num_sms()));
+}
+
+int64_t preft_xchg_region_bytes(int32_t tp_size, int32_t planes, int32_t T_cap, int32_t U_cap) {
+    if (tp_size < 1 || tp_size > PREFT_XCHG_MAX_TP || planes < 1 || T_cap < 1 || U_cap < 1) return 0;
+    return xchg_region_bytes(tp_size, planes, T_cap, U_cap);
+}
+
+int preft_xchg_init(preft_xchg_t* xg, void* const* region_bases, int32_t tp_size, int32_t tp_rank, int32_t planes,
+                    int32_t T_cap, int32_t U_cap, int32_t peer_sys) {
+    return xchg_init(xg, region_bases, tp_size, tp_rank, planes, T_cap, U_cap, peer_sys);
+}
+
+int preft_lora_fused(const preft_meta_t* meta, const void* x, int64_t rows, int64_t ldx, int32_t m,
+                     const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype,
+                     const preft_xchg_t* xchg, void* stream) {
+    return finish(lora_fused(meta, x, rows, ldx, m, sites, nsites, r_max, dtype, xchg,
+                             static_cast<cudaStream_t>(stream), current_num_sms()));
+}
+
+int preft_xchg_errors(const preft_xchg_t* xchg, void* stream, int32_t* out) {
+    return finish(xchg_errors(xchg, static_cast<cudaStream_t>(stream), out));
+}
+
+int preft_dev_alloc(int64_t bytes, void** out) {
+    if (!out || bytes < 1) return PREFT_ERR_SHAPE;
+    *out = nullptr;
+    cudaError_t e = cudaMalloc(out, static_cast<size_t>(bytes));
+    if (e == cudaSuccess) e = cudaMemset(*out, 0, static_cast<size_t>(bytes));
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    return e == cudaSuccess ? PREFT_OK : record_cuda(e);
+}
+
+int preft_dev_free(void* p) {
+    const cudaError_t e = cudaFree(p);
+    return e == cudaSuccess ? PREFT_OK : record_cuda(e);
+}
+
+int preft_ipc_handle(void* dev_ptr, void* handle_out) {
+    static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+    if (!dev_ptr || !handle_out) return PREFT_ERR_SHAPE;
+    cudaIpcMemHandle_t h;
+    const cudaError_t e = cudaIpcGetMemHandle(&h, dev_ptr);
+    if (e != cudaSuccess) return record_cuda(e);
+    memcpy(handle_out, &h, sizeof(h));
+    return PREFT_OK;
+}
+
+int preft_ipc_open(const void* handle, void** dev_ptr_out) {
+    if (!handle || !dev_ptr_out) return PREFT_ERR_SHAPE;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    const cudaError_t e = cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess);
+    return e == cudaSuccess ? PREFT_OK : record_cuda(e);
+}
+
+int preft_ipc_close(void* dev_ptr) {
+    const cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    return e == cudaSuccess ? PREFT_OK : record_cuda(e);
 }
 
 int64_t preft_lora_part_floats(const preft_meta_t* meta) {

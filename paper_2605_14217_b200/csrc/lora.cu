@@ -213,6 +213,26 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
                 cudaStream_t stream, int num_sms);
 int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long long rows, const preft_lora_site_t* sites,
                 int nsites, int r, int dtype, cudaStream_t stream, int num_sms);
+long long lora_split_floats(const preft_meta_t* meta);
+long long lora_part_floats_needed(const preft_meta_t* meta);
+int xchg_init(preft_xchg_t* xg, void* const* bases, int tp, int rank, int planes, int T_cap, int U_cap, int peer_sys);
+bool lora_fused_ok(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
+                   int nsites, int r, int dtype);
+int lora_fused(const preft_meta_t* meta, const void* x, long long rows, long long ldx, int m,
+               const preft_lora_site_t* sites, int nsites, int r, int dtype, const preft_xchg_t* xg,
+               cudaStream_t stream, int num_sms);
+
+// fused shrink -> expand (one launch, lora_fused.cu) for the r >= 16 route:
+// opt-in with PREFT_LORA_FUSED=1 — on one GPU the split pair with K-split
+// planes is faster (the fused kernel exists for the tensor-parallel exchange)
+static bool lora_fused_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("PREFT_LORA_FUSED");
+        on = (e && e[0] == '1') ? 1 : 0;
+    }
+    return on == 1;
+}
 
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
                int nsites, int r, int dtype, cudaStream_t stream, int num_sms) {
@@ -231,6 +251,15 @@ int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, co
     // rank-r intermediate in the meta's workspace (T x nsites x r f32, stays
     // in L2 between the two launches).  Both kernels only touch rows of the
     // K1 units, so the TMA bound T_cap never exposes rows beyond the batch.
+    if (lora_variant() != 0 && lora_fused_enabled() && meta->lora_part &&
+        meta->lora_part_floats >= lora_part_floats_needed(meta) && lora_fused_ok(meta, x, ldx, m, sites, nsites, r, dtype)) {
+        // one rank: the exchange region is the tail of the meta's workspace
+        preft_xchg_t xg;
+        void* base = meta->lora_part + lora_split_floats(meta);
+        const int rc = xchg_init(&xg, &base, 1, 0, 4, meta->T_cap, meta->chunk_cap, 0);
+        if (rc) return rc;
+        return lora_fused(meta, x, meta->T_cap, ldx, m, sites, nsites, r, dtype, &xg, stream, num_sms);
+    }
     if (lora_variant() != 0 && lora_tc_route_ok(meta, x, ldx, m, sites, nsites, r, dtype)) {
         const long long ldp = static_cast<long long>(nsites) * r;
         int rc = lora_shrink(meta, x, meta->T_cap, ldx, m, sites, nsites, r, dtype, meta->lora_part, ldp, stream,

@@ -28,42 +28,12 @@
 #include "common.cuh"
 #include "tc.cuh"
 #include "tmap.cuh"
+#include "split.cuh"
 
 namespace preft {
 
 int grid_for(const void* fn, int threads, int num_sms);
 
-struct SplitSite {
-    const void* A;
-    const void* Bt;     // row-major [S][R][n] (SIMT)
-    const void* Bt_tc;  // core-matrix tiled [S][n/8][R/8][8][8] (tensor cores)
-    const void* scale;
-    void* y;
-    long long ldy;
-    int n;
-    int pad;
-};
-
-struct SplitArgs {
-    const void* x;
-    long long ldx;
-    int m;
-    int nsites;
-    SplitSite site[3];
-    void* P;  // [rows][ldp] acc type
-    long long ldp;
-    int slot_base;  // LoRA-class slots are < slot_split (meta->slot_split)
-    int max_planes; // tensor-core shrink: CTAs that may share one unit (1 = whole units)
-    float* planes;  // partial planes p >= 1 at planes + p * plane_stride (row stride ldp)
-    long long plane_stride;
-    int* sync;      // per-unit arrival counters (zero between launches)
-    int flags;      // kSplitTmaStore: the expand stores full chunks by TMA (default: st.global from smem)
-    long long* prof;  // diagnostics: clock64 stamps of CTA 0 (NULL in production)
-    const int2* tokens;
-    const int2* chunks;
-    const int4* units;
-    const int* counters;
-};
 // ---------------------------------------------------------------- SIMT halves
 
 template <typename T, bool VEC, int R, int NS, int U>
@@ -178,158 +148,7 @@ __global__ void __launch_bounds__(256) expand_simt_kernel(const SplitArgs a) {
     }
 }
 
-// ---------------------------------------------------------------- tcgen05 halves
 
-constexpr int kSpU = 64;                  // unit rows (UMMA M)
-constexpr int kSpChunk = PREFT_CHUNK_ROWS;
-constexpr int kSpN = 128;                 // expand block width (UMMA N) of narrow sites
-constexpr int kSpNMax = 256;              // expand block width of sites with n % 256 == 0
-constexpr int kSpAcc = 4;                 // split shrink accumulators = UMMA-issuing warps
-constexpr int kShrinkThreads = 32 * (6 + kSpAcc);
-constexpr int kPps = 4;                   // K panels (64 columns) per shrink item / ring stage
-constexpr int kPlanes = 4;                // max CTAs sharing one unit's shrink (P partial planes)
-constexpr int kSplitTmaStore = 1;
-
-struct SplitMaps {
-    CUtensorMap x;       // x [rows][m] (this rank's columns), 16-row x 64-col boxes
-    CUtensorMap x64;     // the same with 64-row boxes (a unit of 4 contiguous chunks)
-    CUtensorMap A[3];    // A_s [S*R][m], R-row x 64-col boxes
-    CUtensorMap y[3];    // y_s as [panels][rows][64] (make_tmap_bf16_panels), box {64, 16, block/64}
-};
-
-// A unit whose 4 chunks are consecutive rows of one entry loads as ONE 64-row
-// TMA box per panel (a TMA instruction costs ~30-100 cycles to issue).
-__device__ __forceinline__ bool unit_contiguous(const int2* chunks, int4 U) {
-    if (U.z != 4) return false;
-    const int2 c0 = chunks[U.y], c1 = chunks[U.y + 1], c2 = chunks[U.y + 2], c3 = chunks[U.y + 3];
-    return c0.y == kSpChunk && c1.y == kSpChunk && c2.y == kSpChunk && c1.x == c0.x + kSpChunk &&
-           c2.x == c0.x + 2 * kSpChunk && c3.x == c0.x + 3 * kSpChunk;
-}
-
-// ---- cost-balanced work ranges
-//
-// Work items are (unit u, column block c) over the LoRA-class units (K1 lists
-// them first; counters[PREFT_CTR_LORA_UNITS]), c over `nc` blocks of a unit's
-// columns (the expand: every site's output columns; the shrink: the input
-// columns, kPps panels per block).  Item (u, c) costs
-//     width(c) * (alpha * nch_u + beta)        (bytes-equivalent)
-// alpha per column per 16-row chunk (activation traffic), beta per column
-// (the adapter's weights plus a fixed per-item overhead).  The cost ahead of
-// unit u is  W * (alpha * ch0(u) + beta * u)  with ch0(u) = units[u].y, K1's
-// exclusive prefix of chunk counts.  Each CTA takes the items whose start
-// cost falls in its 1/G of the total, found by a two-level parallel search
-// over the units — no host round trip, so the launch stays graph-safe.
-struct Blocks {
-    int nc;        // blocks per unit
-    int nsites;
-    int first[4];  // first block of each site (first[nsites] = nc)
-    int cw[3];     // block width of each site
-    int coff[3];   // first column of each site among the unit's columns
-    long long W;   // columns per unit
-    __device__ __forceinline__ int site(int c) const {
-        int s = 0;
-        while (s + 1 < nsites && c >= first[s + 1]) ++s;
-        return s;
-    }
-    __device__ __forceinline__ long long off(int c) const {
-        const int s = site(c);
-        return coff[s] + static_cast<long long>(c - first[s]) * cw[s];
-    }
-    // first block whose column offset is >= X (nc if none)
-    __device__ __forceinline__ int first_at_least(long long X) const {
-        if (X <= 0) return 0;
-        for (int s = 0; s < nsites; ++s) {
-            const long long last = coff[s] + static_cast<long long>(first[s + 1] - first[s] - 1) * cw[s];
-            if (X <= last) {
-                const long long j = (X - coff[s] + cw[s] - 1) / cw[s];
-                return first[s] + (j > 0 ? static_cast<int>(j) : 0);
-            }
-        }
-        return nc;
-    }
-};
-
-struct CostModel {
-    const int4* units;
-    int nu;
-    int nch_tot;  // chunks of the LoRA-class units (counters[PREFT_CTR_LORA_CHUNKS])
-    long long alpha, beta;
-    int G;  // CTAs sharing the items (CTAs >= G get none)
-    long long tot;
-    __device__ __forceinline__ long long prefix(int u, const Blocks& b) const {
-        const int ch0 = u < nu ? units[u].y : nch_tot;
-        return b.W * (alpha * ch0 + beta * u);
-    }
-    __device__ __forceinline__ void load(const int* counters) {
-        nu = counters[PREFT_CTR_LORA_UNITS];
-        nch_tot = counters[PREFT_CTR_LORA_CHUNKS];
-    }
-    __device__ __forceinline__ long long target(int cta) const { return tot * cta / G; }
-    // the CTA whose share holds cost position S
-    __device__ __forceinline__ int owner(long long S) const {
-        int b = static_cast<int>(S * G / tot);
-        b = b < G - 1 ? b : G - 1;
-        while (b + 1 < G && target(b + 1) <= S) ++b;
-        while (b > 0 && target(b) > S) --b;
-        return b;
-    }
-    // first item of unit u (or u + 1) whose start cost is >= t
-    __device__ __forceinline__ int first_item(int u, long long t, const Blocks& b) const {
-        const long long base = prefix(u, b), per = alpha * units[u].z + beta;
-        const long long X = t > base ? (t - base + per - 1) / per : 0;
-        return u * b.nc + b.first_at_least(X);
-    }
-};
-
-// [k0, k1) of this CTA; every thread of the block must call it
-__device__ void item_range(CostModel& cm, const Blocks& b, int* s_u, int& k0, int& k1) {
-    k0 = k1 = 0;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int nu = cm.nu;
-    if (nu <= 0) return;
-    cm.tot = cm.prefix(nu, b);
-    if (static_cast<int>(blockIdx.x) >= cm.G || cm.tot <= 0) return;
-    const long long t0 = cm.target(blockIdx.x), t1 = cm.target(blockIdx.x + 1);
-    const int step = (nu + nt - 1) / nt;
-    if (tid < 2) s_u[tid] = 0;
-    __syncthreads();
-    int u = tid * step;
-    if (u < nu) {
-        const long long p = cm.prefix(u, b);
-        if (p <= t0) atomicMax(&s_u[0], u);
-        if (p <= t1) atomicMax(&s_u[1], u);
-    }
-    __syncthreads();
-    const int l0 = s_u[0], l1 = s_u[1];
-    __syncthreads();
-    if (tid < step) {
-        u = l0 + tid;
-        if (u < nu && cm.prefix(u, b) <= t0) atomicMax(&s_u[0], u);
-        u = l1 + tid;
-        if (u < nu && cm.prefix(u, b) <= t1) atomicMax(&s_u[1], u);
-    }
-    __syncthreads();
-    k0 = cm.first_item(s_u[0], t0, b);
-    k1 = static_cast<int>(blockIdx.x) + 1 == cm.G ? nu * b.nc : cm.first_item(s_u[1], t1, b);
-}
-
-// ---- shrink
-
-template <int R, int NS>
-struct ShrinkLayout {
-    static constexpr int NSR = NS * R;
-    static constexpr int PANEL = kSpU * 128;               // 64 rows x 64 columns
-    static constexpr int X_BYTES = kPps * PANEL;
-    static constexpr int AP_BYTES = R * 128;
-    static constexpr int STAGE = X_BYTES + kPps * NS * AP_BYTES;  // multiple of 1024
-    static constexpr int STAGES_FIT = (227 * 1024 - 2048) / STAGE;
-    static constexpr int STAGES = STAGES_FIT > 16 ? 16 : STAGES_FIT;
-    static constexpr int SMEM = STAGES * STAGE + 1024;
-    static constexpr int TMEM_COLS = 2 * kSpAcc * NSR <= 256 ? 256 : 512;
-    static_assert(2 * kSpAcc * NSR <= 512, "TMEM budget");
-};
-
-__device__ __forceinline__ void readout_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 // Items are (unit, block of kPps K panels); a CTA accumulates its run of a
 // unit's blocks (a "visit") in TMEM.  When several CTAs share a unit (at most
@@ -370,32 +189,9 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
     tc::pdl_launch_dependents();
 
     // K blocks of kPps panels; with one plane a unit is never split
-    const int NP = a.m / 64;
     Blocks bl;
-    bl.nsites = 1;
-    bl.nc = a.max_planes > 1 ? NP / kPps : 1;
-    bl.cw[0] = bl.nc == 1 ? a.m : 64 * kPps;
-    bl.coff[0] = 0;
-    bl.first[0] = 0;
-    bl.first[1] = bl.nc;
-    bl.W = a.m;
     CostModel cm;
-    cm.units = a.units;
-    cm.load(a.counters);
-    cm.alpha = kSpChunk * 2;                   // x bytes per column per chunk
-    cm.beta = NS * R * 2 + 16;                 // A bytes per column + per-item overhead
-    cm.G = gridDim.x;
-    if (a.max_planes > 1 && cm.nu > 0) {
-        // a unit may span at most max_planes CTAs: cap the CTAs sharing the
-        // work so that one CTA's share is >= max_unit / f, f = max(1,
-        // max_planes - 2) (a unit then meets at most f + 1 CTAs, with one
-        // to spare for the rounding of the share boundaries)
-        const long long tot = cm.prefix(cm.nu, bl);
-        const long long umax = bl.W * (cm.alpha * PREFT_UNIT_CHUNKS + cm.beta);
-        const long long f = a.max_planes > 3 ? a.max_planes - 2 : 1;
-        const long long g = f * tot / umax;
-        cm.G = static_cast<int>(g < 1 ? 1 : g < cm.G ? g : cm.G);
-    }
+    shrink_model(bl, cm, a.units, a.counters, a.m, NS * R, a.max_planes, gridDim.x, a.beta_s);
     int k0, k1;
     // the schedule reads only K1's units and counters, written by a meta
     // build that completed before the first kernel of this PDL chain could
@@ -539,10 +335,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             // which plane: this CTA's index among the CTAs sharing the unit
             int plane = 0, np = 1;
             if (nc > 1) {
-                const long long base = cm.prefix(u, bl), per = cm.alpha * U.z + cm.beta;
-                const int c_first = cm.owner(base), c_last = cm.owner(base + bl.off(nc - 1) * per);
-                plane = static_cast<int>(blockIdx.x) - c_first;
-                np = c_last - c_first + 1;
+                plane = static_cast<int>(blockIdx.x) - unit_first_cta(cm, bl, u);
+                np = unit_pieces(cm, bl, u, U.z);
             }
             const int sb = ub & 1;
             tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
@@ -615,47 +409,6 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
     }
 }
 
-// ---- expand
-
-// EPI = kEpiRmw: y rows come into the ring by TMA, the epilogue adds D in
-// shared memory and stores the rows back.  EPI = kEpiReduce: the ring holds
-// only Bt; the epilogue writes bf16(D) into a staging tile and a TMA
-// reduce-add adds it into y in L2 (rows of a partial chunk beyond the
-// entry's own are padded with -0.0, which leaves any value and the sign of
-// zero unchanged), so y never passes through the SM.
-constexpr int kEpiRmw = 0, kEpiReduce = 1;
-
-template <int R, int NS, int EPI>
-struct ExpandLayout {
-    static constexpr int QS = 4 * kSpChunk * 128;         // one chunk's rows of a block: <= 4 panels x 16 rows x 128 B
-    static constexpr int Y_BYTES = EPI == kEpiRmw ? 4 * QS : 0;  // the y rows of 4 chunks (32 KB)
-    static constexpr int BT_BYTES = kSpNMax * R * 2;
-    static constexpr int STAGE = Y_BYTES + BT_BYTES;      // multiple of 1024
-    static constexpr int V_BYTES = kSpU * R * 2;          // one V (hi or lo) of one site
-    static constexpr int OFF_V = 0;                       // [2 buffers][NS sites][hi, lo]
-    static constexpr int OFF_STG = 4 * NS * V_BYTES;      // reduce staging [2 groups][2 buffers][4 chunks] x QS
-    static constexpr int STG_BYTES = EPI == kEpiReduce ? 2 * 2 * 4 * QS : 0;
-    static constexpr int OFF_RING = OFF_STG + STG_BYTES;  // multiple of 1024
-    static constexpr int STAGES_FIT = (227 * 1024 - 2048 - OFF_RING) / STAGE;
-    static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
-    static constexpr int SMEM = OFF_RING + STAGES * STAGE + 1024;
-    static_assert(STAGES >= 3, "expand ring too shallow");
-};
-
-__device__ __forceinline__ void expand_blocks(Blocks& b, const SplitArgs& a, int nsites) {
-    b.nsites = nsites;
-    b.nc = 0;
-    long long W = 0;
-    for (int s = 0; s < nsites; ++s) {
-        b.first[s] = b.nc;
-        b.cw[s] = a.site[s].n % kSpNMax == 0 ? kSpNMax : kSpN;
-        b.coff[s] = static_cast<int>(W);
-        b.nc += a.site[s].n / b.cw[s];
-        W += a.site[s].n;
-    }
-    b.first[nsites] = b.nc;
-    b.W = W;
-}
 
 // Items are (unit, output block): per item the producer loads the unit's y
 // rows of the block with one 3D TMA box per 16-row chunk (all of the block's
@@ -704,10 +457,11 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     cm.units = a.units;
     cm.load(a.counters);
     cm.alpha = kSpChunk * 4;  // y read + write per column per chunk
-    cm.beta = 2 * R + 16;     // Bt bytes per column + per-item overhead
+    cm.beta = 2 * R + 16 + a.beta_e;  // Bt bytes per column + per-item overhead
     cm.G = gridDim.x;
     int k0, k1;
     item_range(cm, bl, s_u, k0, k1);  // K1's output only: before the wait (see the shrink)
+
     const int nc = bl.nc;
     tc::pdl_wait();  // P and y come from the previous kernels
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1792 + 2 * blockIdx.x] = tc::globaltimer();
@@ -1086,6 +840,7 @@ static int launch_expand(const SplitMaps& maps, const SplitArgs& args, int nsite
 
 static long long* g_split_prof = nullptr;
 void split_set_profile(long long* buf) { g_split_prof = buf; }
+long long* split_profile_buffer() { return g_split_prof; }
 
 static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -1104,8 +859,31 @@ void set_split_variant(int v) { g_split_variant = v; }
 // [T_cap][64] f32 (plane 0 is P itself on the preft_lora_apply route) and
 // one int per unit (the shrink's per-unit arrival counters, kept zero
 // between launches).
+long long xchg_region_bytes(int tp, int planes, int T_cap, int U_cap);
+
+// floats of the split pair's part of meta->lora_part (P / planes / counters)
+long long lora_split_floats(const preft_meta_t* meta) {
+    return (static_cast<long long>(kPlanes) * meta->T_cap * 64 + meta->chunk_cap + 3) / 4 * 4;
+}
+
+// ... followed by the single-rank exchange region of the fused kernel
+// (lora_fused.cu), which the r >= 16 route of preft_lora_apply uses
 long long lora_part_floats_needed(const preft_meta_t* meta) {
-    return static_cast<long long>(kPlanes) * meta->T_cap * 64 + meta->chunk_cap;
+    return lora_split_floats(meta) + (xchg_region_bytes(1, kPlanes, meta->T_cap, meta->chunk_cap) + 3) / 4;
+}
+
+// cost-model overheads (bytes-equivalent per column per item) beyond the
+// defaults: env PREFT_SPLIT_BETA_S / PREFT_SPLIT_BETA_E
+static void split_tuning(SplitArgs& args) {
+    static int bs = -1, be = -1;
+    if (bs < 0) {
+        const char* e = getenv("PREFT_SPLIT_BETA_S");
+        bs = e ? atoi(e) : kBetaS;
+        e = getenv("PREFT_SPLIT_BETA_E");
+        be = e ? atoi(e) : kBetaE;
+    }
+    args.beta_s = bs;
+    args.beta_e = be;
 }
 
 // the shrink's partial planes (p >= 1) and arrival counters, from the meta's
@@ -1188,6 +966,7 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
                 return PREFT_ERR_CONFIG;
         split_planes(args, meta);
         args.prof = g_split_prof;
+        split_tuning(args);
         if (r == 16) {
             if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
             if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
@@ -1220,6 +999,7 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
     SplitArgs args{};
     fill_common(args, meta, sites, nsites, const_cast<void*>(P), ldp);
     args.prof = g_split_prof;
+    split_tuning(args);
     {
         const char* env = getenv("PREFT_SPLIT_TMA_STORE");
         args.flags = (env && env[0] == '1') ? kSplitTmaStore : 0;

@@ -48,6 +48,8 @@ __all__ = [
     "lora_shrink_tp_",
     "lora_expand_tp_",
     "apply_lora_group_tp_",
+    "FusedExchange",
+    "lora_fused_tp_",
 ]
 
 # Llama projections: which side of the base GEMM is split across the TP group
@@ -131,6 +133,118 @@ class SplitWorkspace:
         return self.P[: T * width].view(T, width)
 
 
+class FusedExchange:
+    """The exchange regions of the fused kernel (preft_lora_fused: shrink ->
+    partials to every rank -> expand, one launch per group; see
+    include/preft.h preft_xchg_t and csrc/lora_fused.cu).
+
+    * `FusedExchange.local(meta, pool)`: one rank on one device — the
+      single-GPU path, or one rank's share of a TP group with the exchange
+      omitted (the 1-GPU config-4 measurement);
+    * `FusedExchange.group(meta, pool, group)`: the real TP group — every
+      rank allocates its region (cudaMalloc, zeroed), the 64-byte IPC handles
+      are all-gathered over torch.distributed and every peer's region is
+      mapped, so the kernel stores its partial rows straight into the peers'
+      HBM over NVLink (no NCCL call on the data path);
+    * `FusedExchange.emulated(meta, pool, tp)`: tp ranks' regions on ONE
+      device (tests: the ranks run as concurrent launches on separate
+      streams with a small grid).
+
+    Every rank must issue the same sequence of fused launches on its
+    exchange (the launch count is the flags' tag)."""
+
+    def __init__(self, xg, keep, owned=(), opened=()):
+        self.c = xg
+        self._keep = keep
+        self._owned = list(owned)
+        self._opened = list(opened)
+
+    @staticmethod
+    def _make(meta, bases, tp, rank, planes, peer_sys, grid):
+        from . import _lib
+
+        xg = _lib.PreftXchg()
+        arr = (ctypes.c_void_p * tp)(*bases)
+        _lib.check(_lib.load().preft_xchg_init(ctypes.byref(xg), arr, tp, rank, planes, meta.T_cap, meta.chunk_cap,
+                                               1 if peer_sys else 0), "xchg_init")
+        xg.grid = grid
+        return xg
+
+    @classmethod
+    def region_bytes(cls, meta, tp: int, planes: int) -> int:
+        from . import _lib
+
+        return int(_lib.load().preft_xchg_region_bytes(tp, planes, meta.T_cap, meta.chunk_cap))
+
+    @classmethod
+    def local(cls, meta, pool, planes: int = 4, grid: int = 0):
+        import torch
+
+        n = (cls.region_bytes(meta, 1, planes) + 15) // 16 * 4
+        buf = torch.zeros(n, dtype=torch.float32, device=pool.device)
+        return cls(cls._make(meta, [buf.data_ptr()], 1, 0, planes, False, grid), [buf])
+
+    @classmethod
+    def emulated(cls, meta, pool, tp: int, planes: int = 1, grid: int = 0):
+        """tp exchanges sharing regions on one device (rank r's view is item r)."""
+        import torch
+
+        n = (cls.region_bytes(meta, tp, planes) + 15) // 16 * 4
+        bufs = [torch.zeros(n, dtype=torch.float32, device=pool.device) for _ in range(tp)]
+        bases = [b.data_ptr() for b in bufs]
+        return [cls(cls._make(meta, bases, tp, r, planes, False, grid), bufs) for r in range(tp)]
+
+    @classmethod
+    def group(cls, meta, pool, group=None, planes: int = 1, grid: int = 0):
+        import torch.distributed as dist
+
+        from . import _lib
+
+        lib = _lib.load()
+        tp, rank = pool.tp_size, pool.tp_rank
+        if dist.get_world_size(group) != tp or dist.get_rank(group) != rank:
+            raise ConfigError("the process group does not match the pool's tensor-parallel layout")
+        nbytes = cls.region_bytes(meta, tp, planes)
+        mine = ctypes.c_void_p()
+        _lib.check(lib.preft_dev_alloc(nbytes, ctypes.byref(mine)), "dev_alloc")
+        handle = ctypes.create_string_buffer(64)
+        _lib.check(lib.preft_ipc_handle(mine, handle), "ipc_handle")
+        handles = [None] * tp
+        dist.all_gather_object(handles, bytes(handle.raw), group=group)  # also: every region is zeroed by now
+        bases, opened = [], []
+        for r, h in enumerate(handles):
+            if r == rank:
+                bases.append(mine.value)
+                continue
+            p = ctypes.c_void_p()
+            _lib.check(lib.preft_ipc_open(ctypes.create_string_buffer(h, 64), ctypes.byref(p)), "ipc_open")
+            bases.append(p.value)
+            opened.append(p.value)
+        return cls(cls._make(meta, bases, tp, rank, planes, True, grid), [], owned=[mine.value], opened=opened)
+
+    def errors(self, stream=None) -> int:
+        """state[2] of this rank's region (bit 0: a wait timed out); syncs the stream."""
+        import torch
+
+        from . import _lib
+
+        s = stream if stream is not None else torch.cuda.current_stream()
+        out = ctypes.c_int32()
+        _lib.check(_lib.load().preft_xchg_errors(ctypes.byref(self.c), ctypes.c_void_p(s.cuda_stream),
+                                                 ctypes.byref(out)), "xchg_errors")
+        return int(out.value)
+
+    def close(self) -> None:
+        from . import _lib
+
+        lib = _lib.load()
+        for p in self._opened:
+            lib.preft_ipc_close(ctypes.c_void_p(p))
+        for p in self._owned:
+            lib.preft_dev_free(ctypes.c_void_p(p))
+        self._opened, self._owned, self._keep = [], [], []
+
+
 def _site_array(ys, x, meta, pool, layer, sites):
     from . import _lib
     from .ops import _check_act, row_stride
@@ -201,6 +315,26 @@ def lora_expand_tp_(P, ys, x, meta, pool, layer: int, sites: Sequence[str], stre
     return ys
 
 
+def lora_fused_tp_(ys, x, meta, pool, layer: int, sites: Sequence[str], exchange: FusedExchange, stream=None):
+    """Shrink -> exchange -> expand in one launch (preft_lora_fused): y[:, n-slice]
+    += s * (sum over the exchange's ranks of x[:, m-slice] A_shard^T) B_shard^T."""
+    import torch
+
+    from . import _lib
+    from .ops import row_stride
+
+    arr, shards, rows = _site_array(ys, x, meta, pool, layer, sites)
+    s = stream if stream is not None else torch.cuda.current_stream(pool.device)
+    meta.require_split(pool.slot_split)
+    st = _lib.load().preft_lora_fused(
+        ctypes.byref(meta.c), ctypes.c_void_p(x.data_ptr() + shards[0].x_offset * x.element_size()), rows,
+        row_stride(x), shards[0].m_loc, arr, len(sites), pool.lora_rank, pool.dtype_code,
+        ctypes.byref(exchange.c), ctypes.c_void_p(s.cuda_stream),
+    )
+    _lib.check(st, "lora_fused")
+    return ys
+
+
 def apply_lora_group_tp_(
     ys: Sequence,
     x,
@@ -212,6 +346,7 @@ def apply_lora_group_tp_(
     workspace: SplitWorkspace | None = None,
     stream=None,
     collective: bool = True,
+    exchange: FusedExchange | None = None,
 ):
     """Tensor-parallel y_s[rows] += s_a (x[rows] A_s,a^T) B_s,a^T for 1-3 sites
     sharing x, on this rank's shard of the pool (`pool.tp_rank` of
@@ -220,7 +355,9 @@ def apply_lora_group_tp_(
     module docstring); `group` is the torch.distributed process group of the
     TP ranks (None = default group; no collective when tp_size == 1).
     collective=False skips the all-reduce (single-GPU emulation of one rank's
-    share of the work; the result is then this rank's partial only)."""
+    share of the work; the result is then this rank's partial only).
+    With an `exchange` (FusedExchange) the group runs as ONE fused launch
+    whose partials travel through the exchange instead of NCCL."""
     import torch
 
     ws = workspace if workspace is not None else SplitWorkspace(meta, pool)
@@ -228,8 +365,11 @@ def apply_lora_group_tp_(
     per = max(1, 64 // pool.lora_rank)  # a launch carries <= 64 rank-r columns of P
     if len(sites) > per:
         for i in range(0, len(sites), per):
-            apply_lora_group_tp_(ys[i : i + per], x, meta, pool, layer, sites[i : i + per], group, ws, s, collective)
+            apply_lora_group_tp_(ys[i : i + per], x, meta, pool, layer, sites[i : i + per], group, ws, s, collective,
+                                 exchange)
         return ys
+    if exchange is not None:
+        return lora_fused_tp_(ys, x, meta, pool, layer, sites, exchange, s)
     P = lora_shrink_tp_(ys, x, meta, pool, layer, sites, ws, s)
     if pool.tp_size > 1 and collective:
         import torch.distributed as dist

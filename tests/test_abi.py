@@ -50,14 +50,18 @@ def test_ctypes_structs_match_c_layout(tmp_path):
         'printf("%zu %zu %zu %zu\\n", sizeof(preft_meta_t), offsetof(preft_meta_t, E_cap),'
         " offsetof(preft_meta_t, slot_split), sizeof(preft_lora_site_t));\n"
         'printf("%zu %zu %zu\\n", offsetof(preft_lora_site_t, bias), offsetof(preft_lora_site_t, ldy),'
-        " offsetof(preft_lora_site_t, n));\nreturn 0;}\n"
+        " offsetof(preft_lora_site_t, n));\n"
+        'printf("%zu %zu %zu %zu\\n", sizeof(preft_xchg_t), offsetof(preft_xchg_t, part),'
+        " offsetof(preft_xchg_t, state), offsetof(preft_xchg_t, spin_ns));\nreturn 0;}\n"
     )
     exe = tmp_path / "layout"
     subprocess.run(["gcc", "-I", str(ROOT / "include"), str(src), "-o", str(exe)], check=True)
     out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     M, S = _lib.PreftMeta, _lib.PreftLoraSite
     assert [int(v) for v in out[:4]] == [ctypes.sizeof(M), M.E_cap.offset, M.slot_split.offset, ctypes.sizeof(S)]
-    assert [int(v) for v in out[4:]] == [S.bias.offset, S.ldy.offset, S.n.offset]
+    assert [int(v) for v in out[4:7]] == [S.bias.offset, S.ldy.offset, S.n.offset]
+    X = _lib.PreftXchg
+    assert [int(v) for v in out[7:]] == [ctypes.sizeof(X), X.part.offset, X.state.offset, X.spin_ns.offset]
 
 
 def test_status_codes_map_to_reference_exceptions():
