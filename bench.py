@@ -72,6 +72,9 @@ def parse(argv=None):
     p.add_argument("--no-parity", action="store_true", help="skip the post-timing parity checks")
     p.add_argument("--only", default="", help="comma list of secondary lines to run alone: "
                    "cfg1,cfg3,cfg5,cfg5s,cfg4,serving,punica,lora16 (skips the headline)")
+    p.add_argument("--tp-exchange", choices=["fused", "nccl"], default="fused",
+                   help="config 4 on a real TP group: the fused kernel's P2P exchange (default) or "
+                        "shrink + NCCL all-reduce + expand")
     p.add_argument("--dry-run", action="store_true",
                    help="CPU/gloo launcher check: routing + collectives + the JSON line, no kernels")
     return p.parse_args(argv)
@@ -908,7 +911,7 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
     from paper_2605_14217_b200 import AdapterKind, costs, shapes
     from paper_2605_14217_b200.meta import BatchMeta
     from paper_2605_14217_b200.pool import AdapterPool
-    from paper_2605_14217_b200.tp import SplitWorkspace, apply_lora_group_tp_
+    from paper_2605_14217_b200.tp import FusedExchange, SplitWorkspace, apply_lora_group_tp_
 
     tp = 8
     if world not in (1, tp):
@@ -939,12 +942,25 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
             acts[group] = (x, ys)
         sets.append(acts)
 
-    def step(s):
+    # on a real TP group the partials travel through the fused kernel's
+    # cudaIpc exchange (no NCCL call on the data path) unless --tp-exchange nccl
+    ex, exchange = None, "NCCL all-reduce of the rank-r partials between the shrink and expand kernels"
+    if real and args.tp_exchange == "fused":
+        try:
+            ex = FusedExchange.group(meta, pool)
+            exchange = "fused kernel: partials stored into every rank's exchange region over NVLink (cudaIpc)"
+        except Exception as exc:  # keep the NCCL path measurable
+            exchange += f" (fused exchange unavailable: {type(exc).__name__}: {exc})"
+    if not real:
+        exchange = "omitted (1 GPU)"
+
+    def step(s, fused_ex=None):
         for layer in range(shape.n_layers):
             acts = sets[layer % 2]
             for group in shapes.SITE_GROUPS:
                 x, ys = acts[group]
-                apply_lora_group_tp_(ys, x, meta, pool, layer, group, workspace=ws, stream=s, collective=real)
+                apply_lora_group_tp_(ys, x, meta, pool, layer, group, workspace=ws, stream=s, collective=real,
+                                     exchange=fused_ex if fused_ex is not None else ex)
 
     s = torch.cuda.current_stream(device)
     for _ in range(2):
@@ -995,7 +1011,33 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
            "prefill_tokens": sel, "ms_per_step": round(ms, 3), "value": round(sel / (ms / 1e3), 1), "unit": UNIT,
            "per_rank_frac_of_hbm_peak": round(frac, 4), "per_rank_algorithmic_bytes": int(step_bytes),
            "allreduce_bytes_per_rank_per_step": int(allreduce_bytes) if real else 0,
-           "pool_gb_per_rank": round(pool.nbytes / 1e9, 2), "launch": launch}
+           "pool_gb_per_rank": round(pool.nbytes / 1e9, 2), "launch": launch, "exchange": exchange}
+    if not real:
+        # the fused shrink -> exchange -> expand kernel that a real TP group
+        # runs, on rank 0's shard with a one-rank exchange (its remote stores
+        # and waits omitted like the all-reduce above)
+        exl = FusedExchange.local(meta, pool, planes=1)
+        fg = torch.cuda.CUDAGraph()
+        step(s, exl)
+        torch.cuda.synchronize()
+        cs2 = torch.cuda.Stream(device)
+        cs2.wait_stream(s)
+        with torch.cuda.stream(cs2), torch.cuda.graph(fg, stream=cs2):
+            step(cs2, exl)
+        s.wait_stream(cs2)
+        fg.replay()
+        torch.cuda.synchronize()
+        e0.record(s)
+        for _ in range(steps):
+            fg.replay()
+        e1.record(s)
+        torch.cuda.synchronize()
+        fms = e0.elapsed_time(e1) / steps
+        out["fused_kernel"] = {"ms_per_step": round(fms, 3), "per_rank_frac_of_hbm_peak":
+                               round(step_bytes / (fms / 1e3) / 1e9 / peak, 4), "launches_per_step": 320,
+                               "note": "the kernel a real TP group runs (one launch per group and layer), "
+                                       "exchange stores to peers omitted on 1 GPU"}
+        del fg, exl
     if not args.no_parity and not real:
         # one more replay: set 0 takes the even layers' deltas (rank 0's partial
         # shrink over its m-slice, its n-slice of B; no all-reduce on 1 GPU)
@@ -1033,6 +1075,10 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
     elif real:
         out["parity"] = {"status": "not checked on the multi-rank run (the kernels' TP=8 parity is "
                                    "tests/test_gpu_tp.py at 70B shard widths)"}
+    if ex is not None:
+        out["exchange_errors"] = ex.errors()
+        barrier(world)
+        ex.close()
     del pool, meta, ws, sets, graph
     torch.cuda.empty_cache()
     return out

@@ -251,8 +251,12 @@ static int reft_colaunch(const preft_meta_t* meta, void* h, long long rows, long
     std::lock_guard<std::mutex> lk(g_co_mu);
     CoStreams* c = co_streams_locked(stream);
     if (!c) return PREFT_ERR_SHAPE;
-    // per-SM rate of the parked kernel ~1.2x the streaming kernel's (no L2 re-read misses)
-    const int f = sp > 0 ? min(4095, sp) : static_cast<int>(4096.0 * 1.2 * g / (1.2 * g + left));
+    // units split in proportion to the kernels' per-SM rates: swept at
+    // config 3 (profiles/reft_cosplit_r02c.txt) the best share of the parked
+    // kernel is 88.5-89% (rate ~0.97x the streaming kernel's per SM; 71.1%
+    // of HBM peak vs 68.8% at the old 1.2x guess); the optimum is sharp
+    // (+-1.5% of the units costs 2-6 points)
+    const int f = sp > 0 ? min(4095, sp) : static_cast<int>(4096.0 * 0.97 * g / (0.97 * g + left));
     if (cudaEventRecord(c->fork, stream) != cudaSuccess) return PREFT_ERR_CONFIG;
     if (cudaStreamWaitEvent(c->aux, c->fork, 0) != cudaSuccess) return PREFT_ERR_CONFIG;
     int rc = reft_res_apply(meta, h, rows, ldh, d, A, Bt, bias, scale, r, stream, num_sms, 0, f, false);
