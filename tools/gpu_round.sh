@@ -44,10 +44,18 @@ timeout 300 ncu --set full --clock-control none --import-source on -k regex:reft
   python tools/reft_bench.py --case cfg3 --variant tc --iters 1 > /dev/null 2>&1
 timeout 400 ncu --set full --clock-control none -k regex:"shrink_tc|expand_tc" -s 8 -c 8 -o $O/${TAG}_split_prof \
   python bench.py --only cfg4 --no-parity --steps 1 > /dev/null 2>&1
+# config 5's K3-TC (LoReFT r32, the whole kernel on 148 SMs), config 3's parked half at d = 4096, and the
+# fused TP kernel at config-4 shapes (q/k/v group, one-rank exchange)
+timeout 300 ncu --set full --clock-control none -k regex:reft_tc -s 3 -c 1 -o $O/${TAG}_cfg5_prof \
+  python tools/reft_bench.py --case cfg5 --variant tc --iters 1 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none -k regex:reft_res -s 3 -c 1 -o $O/${TAG}_res4k_prof \
+  python tools/reft_bench.py --case cfg3 --variant tc --iters 1 > /dev/null 2>&1
+timeout 300 ncu --set full --clock-control none -k regex:lora_fused -s 4 -c 2 -o $O/${TAG}_fused_prof \
+  env GROUP=qkv python tools/fused_prof.py > /dev/null 2>&1
 # full reports are large (the 64 MiB return limit): keep CSV exports of the secondary captures
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:reft_res -s 3 -c 1 -o $O/${TAG}_res_prof \
   python tools/reft_bench.py --case cfg3 --variant res --d 2048 --iters 1 > /dev/null 2>&1
-for r in reft_prof split_prof res_prof; do
+for r in reft_prof split_prof res_prof cfg5_prof res4k_prof fused_prof; do
   ncu -i $O/${TAG}_${r}.ncu-rep --page raw --csv > $O/${TAG}_${r}_raw.csv 2>/dev/null
   python tools/ncu_metrics.py $O/${TAG}_${r}.ncu-rep > $O/${TAG}_${r}_metrics.txt 2>/dev/null
   rm -f $O/${TAG}_${r}.ncu-rep
