@@ -75,6 +75,10 @@ def parse(argv=None):
     p.add_argument("--tp-exchange", choices=["fused", "nccl"], default="fused",
                    help="config 4 on a real TP group: the fused kernel's P2P exchange (default) or "
                         "shrink + NCCL all-reduce + expand")
+    p.add_argument("--share-gpu", action="store_true",
+                   help="functional check of the multi-rank path on a 1-GPU box: every rank on cuda:0, gloo "
+                        "for the bookkeeping collectives; the ranks time-share the GPU, so the numbers are not "
+                        "scaling measurements")
     p.add_argument("--dry-run", action="store_true",
                    help="CPU/gloo launcher check: routing + collectives + the JSON line, no kernels")
     return p.parse_args(argv)
@@ -1294,11 +1298,21 @@ def secondary_lines(args, device, world: int, rank: int, only: set[str]) -> list
     return out
 
 
+SHARED_NOTE = ("every rank on ONE GPU (--share-gpu): a functional run of the multi-rank path (launcher, "
+               "adapter sharding, request routing, per-rank kernels, max-over-ranks timing); the ranks time-share "
+               "the GPU, so the values are not scaling measurements")
+
+
 def run_ours(args):
     import torch
 
     world, rank, local = dist_setup(args)
-    dist_init(world, local)
+    if args.share_gpu and world > 1:
+        local = 0
+        torch.cuda.set_device(0)
+        dist_init(world, local, backend="gloo")
+    else:
+        dist_init(world, local)
     device = torch.device("cuda", local)
     only = {k for k in args.only.split(",") if k}
     if only:
@@ -1307,7 +1321,10 @@ def run_ours(args):
             others.append(punica_step(args, rank, world, device))
         others += secondary_lines(args, device, world, rank, only)
         if rank == 0:
-            print(json.dumps({"metric": METRIC, "only": sorted(only), "n_gpus": world, "other_configs": others}))
+            line = {"metric": METRIC, "only": sorted(only), "n_gpus": world, "other_configs": others}
+            if args.share_gpu and world > 1:
+                line["shared_gpu"] = SHARED_NOTE
+            print(json.dumps(line))
         if world > 1:
             torch.distributed.destroy_process_group()
         return
@@ -1396,6 +1413,8 @@ def run_ours(args):
             "punica_step": punica,
             "other_configs": others,
         }
+        if args.share_gpu and world > 1:
+            line["shared_gpu"] = SHARED_NOTE
         print(json.dumps(line))
     if world > 1:
         import torch.distributed as dist

@@ -58,3 +58,19 @@ def test_reference_arm_same_config_as_ours(tmp_path):
     qsl, ids, flags, lens, _ = bench.step_entries(0, 1, 6, 4)
     assert line["config"]["prefill_tokens_per_gpu"] == int(lens.sum())
     assert line["config"]["workload"].startswith("cfg2")
+
+
+@pytest.mark.gpu
+def test_gpus_2_on_one_gpu_runs_the_multi_rank_path():
+    """The multi-rank path with real kernels on a 1-GPU box: `bench.py --gpus 2
+    --share-gpu` self-launches two ranks on cuda:0 (gloo bookkeeping); the
+    config-5 strong-scaling line routes one global Zipf stream to the adapter
+    owners with the head adapter replicated, and its parity must pass."""
+    r = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--share-gpu", "--steps", "2",
+                        "--warmup", "3", "--only", "cfg5s"], capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = _last_json(r.stdout)
+    assert line["n_gpus"] == 2 and "shared_gpu" in line
+    (c,) = line["other_configs"]
+    assert c["n_gpus"] == 2 and c["parity"]["status"] == "pass"
+    assert c["hot_replicated_adapters"] == [0] and len(c["requests_per_rank"]) == 2
