@@ -50,7 +50,7 @@ timeout 300 ncu --set full --clock-control none -k regex:reft_tc -s 3 -c 1 -o $O
   python tools/reft_bench.py --case cfg5 --variant tc --iters 1 > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none -k regex:reft_res -s 3 -c 1 -o $O/${TAG}_res4k_prof \
   python tools/reft_bench.py --case cfg3 --variant tc --iters 1 > /dev/null 2>&1
-timeout 300 ncu --set full --clock-control none -k regex:lora_fused -s 4 -c 2 -o $O/${TAG}_fused_prof \
+timeout 300 ncu --set full --clock-control none -k regex:lora_fused -s 2 -c 1 -o $O/${TAG}_fused_prof \
   env GROUP=qkv python tools/fused_prof.py > /dev/null 2>&1
 # full reports are large (the 64 MiB return limit): keep CSV exports of the secondary captures
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:reft_res -s 3 -c 1 -o $O/${TAG}_res_prof \
