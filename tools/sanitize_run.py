@@ -1,6 +1,6 @@
 #!/usr/bin/env python
 """Small invocations of every kernel family for compute-sanitizer runs:
-K1, K2 (team, warp, f64), K2 split (tcgen05 + SIMT), K3 (SIMT + tcgen05 streaming +
+K1, K2 (team, warp, f64), K2 split (tcgen05 + SIMT), K2f (fused, one-rank exchange), K3 (SIMT + tcgen05 streaming +
 tcgen05 TMEM-parked at d = 1024 / 2048), K4."""
 import sys
 from pathlib import Path
@@ -44,6 +44,16 @@ def main():
         h = U.rand_act(rng, T, d, dtype, dev)
         apply_lora_group_(ys, x, meta, pool, 0, tuple(sites))
         apply_lora_group_tp_(ys, x, meta, pool, 0, tuple(sites), workspace=SplitWorkspace(meta, pool))
+        if dtype == torch.bfloat16 and lr == 16:
+            # K2f, the fused shrink -> exchange -> expand kernel, one rank, whole and K-split units
+            from paper_2605_14217_b200.tp import FusedExchange
+
+            for planes in (1, 4):
+                ex = FusedExchange.local(meta, pool, planes=planes)
+                for _ in range(2):  # both parities
+                    apply_lora_group_tp_(ys, x, meta, pool, 0, tuple(sites), exchange=ex)
+                torch.cuda.synchronize()
+                assert ex.errors() == 0
         apply_reft_(h, meta, pool, 0)
         torch.cuda.synchronize()
         print("ok", dtype, lr, rr)
