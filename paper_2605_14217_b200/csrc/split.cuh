@@ -36,6 +36,8 @@ struct SplitArgs {
     long long plane_stride;
     int* sync;      // per-unit arrival counters (zero between launches)
     int flags;      // kSplitTmaStore: the expand stores full chunks by TMA (default: st.global from smem)
+    int* sched;     // dynamic expand: [0] next grab, [1] finished CTAs (zero between launches); NULL = static ranges
+    int grab;       // items per grab
     int beta_s;     // added to the shrink / expand cost models' per-column item overhead
     int beta_e;     //   (tuning; env PREFT_SPLIT_BETA_S / _E)
     long long* prof;  // diagnostics: clock64 stamps of CTA 0 (NULL in production)
@@ -62,6 +64,8 @@ constexpr int kPlanes = 4;                // max CTAs sharing one unit's shrink 
 constexpr int kBetaS = 128;
 constexpr int kBetaE = 128;
 constexpr int kSplitTmaStore = 1;
+constexpr int kSplitHints = 2;
+constexpr int kSchedInts = 8;  // expand: Bt loads evict_last, y reduce-adds evict_first
 
 struct SplitMaps {
     CUtensorMap x;       // x [rows][m] (this rank's columns), 16-row x 64-col boxes

@@ -239,6 +239,25 @@ __device__ __forceinline__ void tma_reduce_add_3d(const void* tmap, int c0, int 
                  : "memory");
 }
 
+__device__ __forceinline__ void tma_reduce_add_3d_hint(const void* tmap, int c0, int c1, int c2, uint32_t ssrc,
+                                                       uint64_t policy) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group.L2::cache_hint [%0, {%1, %2, %3}], "
+        "[%4], %5;" ::"l"(reinterpret_cast<uint64_t>(tmap)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(ssrc), "l"(policy)
+        : "memory");
+}
+
+// bulk copy with an L2 cache hint
+__device__ __forceinline__ void bulk_load_1d_hint(uint32_t sdst, const void* gsrc, uint32_t bytes, uint64_t* mbar,
+                                                  uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(sdst),
+        "l"(reinterpret_cast<uint64_t>(gsrc)), "r"(bytes), "r"(smem_u32(mbar)), "l"(policy)
+        : "memory");
+}
+
 // contiguous global -> shared bulk copy (bytes % 16 == 0, 16 B aligned), completion on an mbarrier
 __device__ __forceinline__ void bulk_load_1d(uint32_t sdst, const void* gsrc, uint32_t bytes, uint64_t* mbar) {
     asm volatile(
