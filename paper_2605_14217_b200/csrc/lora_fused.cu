@@ -36,6 +36,7 @@
 
 #include "common.cuh"
 #include "split.cuh"
+#include "expand.cuh"
 #include "tc.cuh"
 #include "tmap.cuh"
 
@@ -49,8 +50,10 @@ struct XchgArgs {
     int T_cap, U_cap;
     long long spin_ns;
     int beta_s, beta_e;  // cost-model tuning (env PREFT_FUSED_BETA_S / _E)
-    int knobs;           // experiments: bit 0 no producer fence, bit 1 no consumer fence
+    int knobs;           // experiments: bit 0 no producer fence
+    int dyn, grab;       // phase 2: dynamic item grabs (state[3] is the counter), items per grab
 };
+
 
 __host__ __device__ __forceinline__ long long xchg_part_off(int par, int src, int plane, int tp, int planes, int T_cap) {
     return ((static_cast<long long>(par) * tp + src) * planes + plane) * T_cap * 64;
@@ -74,17 +77,75 @@ __device__ __forceinline__ int ld_flag(const int* p, bool sys) {
         asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void fence_sc(bool sys) {
+// release fence of the publishing lane: it follows the readout warps' partial
+// stores through the named barrier, so a cumulative acq_rel fence orders all
+// of them before the flag store
+__device__ __forceinline__ void fence_release(bool sys) {
     if (sys)
-        asm volatile("fence.sc.sys;" ::: "memory");
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
     else
-        asm volatile("fence.sc.gpu;" ::: "memory");
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
+
+// phase 2's rank-r rows: wait for every (source rank, piece) flag of the
+// unit, then sum the partials in (source, piece) order — the same order on
+// every rank, so every rank's V is bit-identical, like an all-reduce's
+struct XchgVSrc {
+    const float* part;  // this rank's region
+    const int* flag;
+    int* state;
+    const CostModel* cs;
+    const Blocks* bs;
+    int tp, planes, T_cap, U_cap, par, tag;
+    bool sys;
+    long long spin_ns;
+    int npc;
+    __device__ __forceinline__ void prepare(int u, const int4& U) {
+        const int lane = threadIdx.x & 31;
+        npc = unit_pieces(*cs, *bs, u, U.z);
+        const int nflags = tp * npc;
+        bool ok = lane >= nflags;
+        const int* fp = ok ? nullptr : flag + xchg_flag_off(par, lane / npc, lane % npc, u, tp, planes, U_cap);
+        uint64_t t0 = 0;
+        while (true) {
+            if (!ok) ok = ld_flag(fp, sys) == tag;
+            if (__all_sync(0xffffffffu, ok)) break;
+            const uint64_t now = tc::globaltimer();
+            if (t0 == 0) t0 = now;
+            if (static_cast<long long>(now - t0) > spin_ns) {
+                if (lane == 0) atomicOr(state + 2, 1);
+                break;
+            }
+            __nanosleep(64);
+        }
+        // every flag was read with ld.acquire by some lane; the warp barrier
+        // orders the other lanes' partial loads after those acquires
+        __syncwarp();
+    }
+    __device__ __forceinline__ void load(long long row, int col, float4& p0, float4& p1) const {
+        p0 = make_float4(0.f, 0.f, 0.f, 0.f);
+        p1 = p0;
+        for (int src = 0; src < tp; ++src)
+            for (int pl = 0; pl < npc; ++pl) {
+                const float* pr = part + xchg_part_off(par, src, pl, tp, planes, T_cap) + row * 64 + col;
+                const float4 w0 = __ldcg(reinterpret_cast<const float4*>(pr));
+                const float4 w1 = __ldcg(reinterpret_cast<const float4*>(pr + 4));
+                p0.x += w0.x;
+                p0.y += w0.y;
+                p0.z += w0.z;
+                p0.w += w0.w;
+                p1.x += w1.x;
+                p1.y += w1.y;
+                p1.z += w1.z;
+                p1.w += w1.w;
+            }
+    }
+};
 
 template <int R, int NS>
 struct FusedLayout {
     using LS = ShrinkLayout<R, NS>;
-    using LE = ExpandLayout<R, NS, kEpiReduce>;
+    using LE = ExpandLayout<R, NS>;
     static constexpr int SMEM = LS::SMEM > LE::SMEM ? LS::SMEM : LE::SMEM;
 };
 
@@ -95,11 +156,13 @@ template <int R, int NS>
 __global__ void __launch_bounds__(384, 1)
     lora_fused_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a, const XchgArgs xa) {
     using LS = ShrinkLayout<R, NS>;
-    using LE = ExpandLayout<R, NS, kEpiReduce>;
+    using LE = ExpandLayout<R, NS>;
     extern __shared__ unsigned char sm_raw[];
     __shared__ __align__(8) uint64_t full[LS::STAGES], empty[LS::STAGES], s_full[2], s_empty[2];
     __shared__ __align__(8) uint64_t efull[LE::STAGES], eempty[LE::STAGES];
     __shared__ __align__(8) uint64_t v_full[2], v_empty[2], d_full[2], d_empty[2];
+    __shared__ __align__(8) uint64_t q_full[kExpQ], q_empty[kExpQ];
+    __shared__ int q_lo[kExpQ], q_hi[kExpQ];
     __shared__ uint32_t tslot;
     __shared__ int s_u[2];
     __shared__ int s_tag;
@@ -107,6 +170,7 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t raw = tc::smem_u32(sm_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
     unsigned char* sgen = sm_raw + (sbase - raw);
+    const ExpandBars EB{efull, eempty, v_full, v_empty, d_full, d_empty, q_full, q_empty, q_lo, q_hi};
     if (warp == 0) tc::tmem_alloc(&tslot, 512);
     if (tid == 32) {
         for (int i = 0; i < LS::STAGES; ++i) {
@@ -117,16 +181,7 @@ __global__ void __launch_bounds__(384, 1)
             tc::mbar_init(&s_full[b], kSpAcc);
             tc::mbar_init(&s_empty[b], 4);
         }
-        for (int i = 0; i < LE::STAGES; ++i) {
-            tc::mbar_init(&efull[i], 1);
-            tc::mbar_init(&eempty[i], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&v_full[b], 2);
-            tc::mbar_init(&v_empty[b], 1);
-            tc::mbar_init(&d_full[b], 1);
-            tc::mbar_init(&d_empty[b], 4);
-        }
+        expand_bars_init(EB, LE::STAGES);
         tc::fence_mbar_init();
         tc::prefetch_tmap(&maps.x);
     }
@@ -317,7 +372,7 @@ __global__ void __launch_bounds__(384, 1)
             // publish the piece once all four quadrants' rows are stored
             readout_bar();
             if (warp == 2 && lane < xa.tp) {
-                if (!(xa.knobs & 1)) fence_sc(sys);
+                if (!(xa.knobs & 1)) fence_release(sys);
                 st_flag(xa.flag[lane] + xchg_flag_off(par, xa.rank, plane, u, xa.tp, xa.planes, xa.U_cap), tag, sys);
             }
             ++ub;
@@ -329,207 +384,11 @@ __global__ void __launch_bounds__(384, 1)
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1537 + 2 * blockIdx.x] = tc::globaltimer();
 
     // ================================================================ phase 2: expand
-    if (warp == 0) {
-        int stage = 0, pu = -1, slot = 0;
-        uint32_t phase = 0;
-        for (int k = e0; k < e1; ++k) {
-            const int u = k / nce, c = k - u * nce;
-            if (u != pu) {
-                slot = a.units[u].x;
-                pu = u;
-            }
-            const int s = be.site(c), j = c - be.first[s], cw = be.cw[s];
-            const uint32_t bt_bytes = static_cast<uint32_t>(cw * R * 2);
-            if (lane == 0) {
-                tc::mbar_wait(&eempty[stage], phase ^ 1u);
-                tc::mbar_expect_tx(&efull[stage], bt_bytes);
-                tc::bulk_load_1d(sbase + LE::OFF_RING + stage * LE::STAGE,
-                                 static_cast<const unsigned char*>(a.site[s].Bt_tc) +
-                                     static_cast<long long>(slot) * a.site[s].n * R * 2 +
-                                     static_cast<long long>(j) * bt_bytes,
-                                 bt_bytes, &efull[stage]);
-            }
-            __syncwarp();
-            if (++stage == LE::STAGES) {
-                stage = 0;
-                phase ^= 1u;
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t id128 = tc::idesc_bf16_f32(kSpU, kSpN), id256 = tc::idesc_bf16_f32(kSpU, kSpNMax);
-            int stage = 0, visit = 0;
-            uint32_t phase = 0;
-            for (int k = e0; k < e1; ++k) {
-                const int u = k / nce, c = k - u * nce, jt = k - e0;
-                const int vb = visit & 1;
-                if (k == e0 || c == 0) {
-                    tc::mbar_wait(&v_full[vb], (visit >> 1) & 1);
-                    tc::fence_after_sync();
-                }
-                const int s = be.site(c);
-                const uint32_t vhi = sbase + LE::OFF_V + ((vb * NS + s) * 2) * LE::V_BYTES, vlo = vhi + LE::V_BYTES;
-                tc::mbar_wait(&efull[stage], phase);
-                const int db = jt & 1;
-                tc::mbar_wait(&d_empty[db], ((jt >> 1) & 1) ^ 1u);
-                tc::fence_after_sync();
-                const uint32_t bt = sbase + LE::OFF_RING + stage * LE::STAGE;
-                const uint32_t dD = tmem + db * kSpNMax;
-                const uint32_t id = be.cw[s] == kSpNMax ? id256 : id128;
-#pragma unroll
-                for (int kk = 0; kk < R / 16; ++kk) {
-                    const uint64_t bd = tc::desc_kmajor(bt + kk * 256, 128, R * 16);
-                    tc::mma_bf16(dD, tc::desc_kmajor(vhi + kk * 256, 128, R * 16), bd, id, kk > 0 ? 1u : 0u);
-                    tc::mma_bf16(dD, tc::desc_kmajor(vlo + kk * 256, 128, R * 16), bd, id, 1u);
-                }
-                tc::mma_commit(&d_full[db]);
-                tc::mma_commit(&eempty[stage]);
-                if (++stage == LE::STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-                if (k + 1 == e1 || c + 1 == nce) {
-                    tc::mma_commit(&v_empty[vb]);
-                    ++visit;
-                }
-            }
-        }
-    } else if (warp < 4) {
-        // wait for every (rank, piece) of the unit, then V = scale * sum
-        int visit = 0;
-        const int* myflag = xa.flag[xa.rank];
-        const float* mypart = xa.part[xa.rank];
-        for (int k = e0; k < e1; ++k) {
-            const int u = k / nce;
-            if (!(k == e0 || k == u * nce)) continue;
-            const int4 U = a.units[u];
-            const int npc = unit_pieces(cs, bs, u, U.z);
-            const int nflags = xa.tp * npc;
-            {
-                bool ok = lane >= nflags;
-                const int* fp = ok ? nullptr
-                                   : myflag + xchg_flag_off(par, lane / npc, lane % npc, u, xa.tp, xa.planes, xa.U_cap);
-                uint64_t t0 = 0;
-                while (true) {
-                    if (!ok) ok = ld_flag(fp, sys) == tag;
-                    if (__all_sync(0xffffffffu, ok)) break;
-                    const uint64_t now = tc::globaltimer();
-                    if (t0 == 0) t0 = now;
-                    if (static_cast<long long>(now - t0) > xa.spin_ns) {
-                        if (lane == 0) atomicOr(xa.state + 2, 1);
-                        break;
-                    }
-                    __nanosleep(64);
-                }
-                if (!(xa.knobs & 2)) fence_sc(sys);
-            }
-            if (a.prof && visit == 0 && warp == 2 && lane == 0 && blockIdx.x < 128)
-                a.prof[1793 + 2 * blockIdx.x] = tc::globaltimer();
-            const int vb = visit & 1;
-            const int m = (warp - 2) * 32 + lane, q = m >> 4, rr = m & 15;
-            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-            const bool valid = rr < ch.y;
-            const long long rowoff = static_cast<long long>(ch.x + rr) * 64;
-            tc::mbar_wait(&v_empty[vb], ((visit >> 1) & 1) ^ 1u);
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                const float sc = __ldg(static_cast<const float*>(a.site[s].scale) + U.x);
-                unsigned char* vhi = sgen + LE::OFF_V + ((vb * NS + s) * 2) * LE::V_BYTES;
-#pragma unroll
-                for (int k0v = 0; k0v < R; k0v += 8) {
-                    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
-                    if (valid) {
-                        for (int src = 0; src < xa.tp; ++src)
-                            for (int pl = 0; pl < npc; ++pl) {
-                                const float* pr = mypart + xchg_part_off(par, src, pl, xa.tp, xa.planes, xa.T_cap) +
-                                                  rowoff + s * R + k0v;
-                                const float4 w0 = __ldcg(reinterpret_cast<const float4*>(pr));
-                                const float4 w1 = __ldcg(reinterpret_cast<const float4*>(pr + 4));
-                                p0.x += w0.x;
-                                p0.y += w0.y;
-                                p0.z += w0.z;
-                                p0.w += w0.w;
-                                p1.x += w1.x;
-                                p1.y += w1.y;
-                                p1.z += w1.z;
-                                p1.w += w1.w;
-                            }
-                    }
-                    const float v[8] = {p0.x * sc, p0.y * sc, p0.z * sc, p0.w * sc,
-                                        p1.x * sc, p1.y * sc, p1.z * sc, p1.w * sc};
-                    uint32_t hi[4], lo[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        hi[e] = f32x2_to_bf16(v[2 * e], v[2 * e + 1]);
-                        float h0, h1;
-                        bf16x2_to_acc(hi[e], h0, h1);
-                        lo[e] = f32x2_to_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
-                    }
-                    const uint32_t off = tc::kmajor_offset(m, k0v, R);
-                    *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                    *reinterpret_cast<uint4*>(vhi + LE::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                }
-            }
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&v_full[vb]);
-            ++visit;
-        }
-    } else {
-        // epilogue group g: D -> bf16 staging tile -> TMA reduce-add into y
-        const int q = warp & 3, g = (warp - 4) >> 2;
-        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-        const int r1 = lane >> 2, cp = 2 * (lane & 3);
-        int pu = -1;
-        int2 ch = make_int2(0, 0);
-        for (int k = e0 + g; k < e1; k += 2) {
-            const int u = k / nce, c = k - u * nce, jt = k - e0;
-            if (u != pu) {
-                const int4 U = a.units[u];
-                ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-                pu = u;
-            }
-            const int s = be.site(c), j = c - be.first[s], cw = be.cw[s], npan = cw / 64;
-            tc::mbar_wait(&d_full[g], (jt >> 1) & 1);
-            tc::fence_after_sync();
-            const int sb = (jt >> 1) & 1;
-            const uint32_t tile = LE::OFF_STG + ((g * 2 + sb) * 4 + q) * LE::QS;
-            if (lane == 0) tc::tma_store_wait_read_1();
-            __syncwarp();
-            if (ch.y > 0) {
-                for (int pass = 0; pass < npan / 2; ++pass) {
-                    uint32_t v[2][32];
-                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128, v[0]);
-                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128 + 64, v[1]);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int pw = 0; pw < 2; ++pw) {
-                        const uint32_t panel = tile + (2 * pass + pw) * (kSpChunk * 128);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half) {
-                                const int r = r1 + 8 * half;
-                                const uint32_t w = r < ch.y ? f32x2_to_bf16(__uint_as_float(v[pw][4 * i + 2 * half]),
-                                                                             __uint_as_float(v[pw][4 * i + 2 * half + 1]))
-                                                            : 0x80008000u;  // -0.0: y + (-0) == y bit for bit
-                                *reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(r, 8 * i + cp, kSpChunk)) = w;
-                            }
-                    }
-                }
-            }
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&d_empty[g]);
-            if (ch.y > 0) {
-                tc::fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) tc::tma_reduce_add_3d(&maps.y[s], 0, ch.x, j * npan, sbase + tile);
-            }
-            if (lane == 0) tc::tma_store_commit();
-            __syncwarp();
-        }
-        if (lane == 0) tc::tma_store_wait_all();
+    {
+        ExpandWork W{e0, e1, xa.dyn ? xa.state + 3 : nullptr, xa.grab, a.counters[PREFT_CTR_LORA_UNITS] * nce};
+        XchgVSrc vs{xa.part[xa.rank], xa.flag[xa.rank], xa.state, &cs, &bs, xa.tp, xa.planes, xa.T_cap, xa.U_cap,
+                    par, tag, sys, xa.spin_ns, 1};
+        expand_pipeline<R, NS>(maps, a, be, sbase, sgen, tmem, EB, W, vs);
     }
     tc::fence_before_sync();
     __syncthreads();
@@ -540,6 +399,7 @@ __global__ void __launch_bounds__(384, 1)
         __threadfence();
         if (atomicAdd(xa.state + 1, 1) == static_cast<int>(gridDim.x) - 1) {
             xa.state[1] = 0;
+            xa.state[3] = 0;  // phase 2's grab counter
             __threadfence();
             atomicExch(xa.state, tag);
         }
@@ -661,6 +521,18 @@ int lora_fused(const preft_meta_t* meta, const void* x, long long rows, long lon
     xa.T_cap = xg->T_cap;
     xa.U_cap = xg->U_cap;
     xa.spin_ns = xg->spin_ns > 0 ? xg->spin_ns : 2000000000ll;
+    {
+        // phase 2's dynamic grabs for the widest groups (>= 64 output blocks per
+        // unit: 8B gate/up, step 14.75 -> 13.98 ms, now level with the split
+        // pair); at 28 blocks (config-4 gate/up) the grabs meet units whose
+        // shrink is still running and lose (12.14 -> 12.75 ms).
+        // PREFT_SPLIT_DYN=0/1 forces off/on.
+        int blocks = 0;
+        for (int s = 0; s < nsites; ++s) blocks += sites[s].n / (sites[s].n % kSpNMax == 0 ? kSpNMax : kSpN);
+        const char* e = getenv("PREFT_SPLIT_DYN");
+        xa.dyn = e ? (e[0] != '0') : blocks >= 64;
+        xa.grab = blocks >= 64 ? 8 : 4;
+    }
     xa.beta_s = kBetaS;
     xa.beta_e = kBetaE;
     if (const char* e = getenv("PREFT_FUSED_BETA_S")) xa.beta_s = atoi(e);

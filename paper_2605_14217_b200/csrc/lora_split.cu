@@ -29,6 +29,7 @@
 #include "tc.cuh"
 #include "tmap.cuh"
 #include "split.cuh"
+#include "expand.cuh"
 
 namespace preft {
 
@@ -410,40 +411,28 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
 }
 
 
-// Items are (unit, output block): per item the producer loads the unit's y
-// rows of the block with one 3D TMA box per 16-row chunk (all of the block's
-// 64-column panels at once) plus the block's Bt by one bulk copy; the MMA
-// warp computes D = V . Bt (hi and lo halves of V) into TMEM buffer
-// (item & 1); the two epilogue groups take alternate items, so two blocks
-// are in their TMEM -> registers -> shared -> TMA-store pipeline at once.
-//
-// warps: 0 TMA producer, 1 UMMA issuer, 2-3 P rows -> bf16 hi/lo V,
-//        4-7 epilogue group 0 (even items), 8-11 group 1 (odd items)
-template <int R, int NS, int EPI>
+// The expand (the pipeline in expand.cuh): static cost-balanced item ranges,
+// or dynamic grabs (a.sched) for wide groups — the static ranges finished at
+// max/mean 1.29 across CTAs at config-4 gate/up although every item ran at
+// the SM's share of HBM.  The last CTA out resets the grab counter.
+template <int R, int NS>
 __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
-    using L = ExpandLayout<R, NS, EPI>;
+    using L = ExpandLayout<R, NS>;
     extern __shared__ unsigned char sm_raw[];
     __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
     __shared__ __align__(8) uint64_t v_full[2], v_empty[2], d_full[2], d_empty[2];
+    __shared__ __align__(8) uint64_t q_full[kExpQ], q_empty[kExpQ];
+    __shared__ int q_lo[kExpQ], q_hi[kExpQ];
     __shared__ uint32_t tslot;
     __shared__ int s_u[2];
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t raw = tc::smem_u32(sm_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
     unsigned char* sgen = sm_raw + (sbase - raw);
+    const ExpandBars B{full, empty, v_full, v_empty, d_full, d_empty, q_full, q_empty, q_lo, q_hi};
     if (warp == 0) tc::tmem_alloc(&tslot, 512);
     if (tid == 32) {
-        for (int i = 0; i < L::STAGES; ++i) {
-            tc::mbar_init(&full[i], 1);
-            // MMA commit (Bt read) [+ the item's 4 epilogue warps (y rows stored)]
-            tc::mbar_init(&empty[i], EPI == kEpiRmw ? 1 + 4 : 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&v_full[b], 2);
-            tc::mbar_init(&v_empty[b], 1);
-            tc::mbar_init(&d_full[b], 1);
-            tc::mbar_init(&d_empty[b], 4);
-        }
+        expand_bars_init(B, L::STAGES);
         tc::fence_mbar_init();
     }
     tc::fence_before_sync();
@@ -453,573 +442,27 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
     tc::pdl_launch_dependents();
     Blocks bl;
     expand_blocks(bl, a, NS);
-    CostModel cm;
-    cm.units = a.units;
-    cm.load(a.counters);
-    cm.alpha = kSpChunk * 4;  // y read + write per column per chunk
-    cm.beta = 2 * R + 16 + a.beta_e;  // Bt bytes per column + per-item overhead
-    cm.G = gridDim.x;
-    int k0, k1;
-    item_range(cm, bl, s_u, k0, k1);  // K1's output only: before the wait (see the shrink)
-
-    const int nc = bl.nc;
-    tc::pdl_wait();  // P and y come from the previous kernels
-    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1792 + 2 * blockIdx.x] = tc::globaltimer();
-
-    if (warp == 0) {
-        // producer: lane q issues chunk q's 3D box, lane 16 the Bt block
-        const uint64_t stream = tc::policy_evict_first();
-        const uint64_t keep = tc::policy_evict_last();  // Bt: reused by the adapter's next unit
-        int stage = 0, npc = 0, pu = -1, row = 0, nch = 0, slot = 0;
-        uint32_t phase = 0;
-        for (int k = k0; k < k1; ++k) {
-            const int u = k / nc, c = k - u * nc;
-            if (u != pu) {
-                const int4 U = a.units[u];
-                nch = U.z;
-                slot = U.x;
-                row = lane < nch ? a.chunks[U.y + lane].x : 0;
-                pu = u;
-            }
-            const int s = bl.site(c), j = c - bl.first[s], cw = bl.cw[s];
-            const uint32_t bt_bytes = static_cast<uint32_t>(cw * R * 2);
-            if (lane == 0) {
-                tc::mbar_wait(&empty[stage], phase ^ 1u);
-                if (a.prof && blockIdx.x == 0 && npc < 128) a.prof[512 + npc * 4 + 0] = clock64();
-                tc::mbar_expect_tx(&full[stage], (EPI == kEpiRmw ? static_cast<uint32_t>(nch * (cw / 64) * kSpChunk * 128) : 0u) +
-                                                     bt_bytes);
-            }
-            ++npc;
-            __syncwarp();
-            const uint32_t st = sbase + L::OFF_RING + stage * L::STAGE;
-            if (EPI == kEpiRmw && lane < nch)
-                tc::tma_load_3d_hint(st + lane * L::QS, &maps.y[s], 0, row, j * (cw / 64), &full[stage], stream);
-            if (lane == 16) {
-                const unsigned char* src = static_cast<const unsigned char*>(a.site[s].Bt_tc) +
-                                           static_cast<long long>(slot) * a.site[s].n * R * 2 +
-                                           static_cast<long long>(j) * bt_bytes;
-                if (a.flags & kSplitHints)
-                    tc::bulk_load_1d_hint(st + L::Y_BYTES, src, bt_bytes, &full[stage], keep);
-                else
-                    tc::bulk_load_1d(st + L::Y_BYTES, src, bt_bytes, &full[stage]);
-            }
-            if (++stage == L::STAGES) {
-                stage = 0;
-                phase ^= 1u;
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            const uint32_t id128 = tc::idesc_bf16_f32(kSpU, kSpN), id256 = tc::idesc_bf16_f32(kSpU, kSpNMax);
-            int stage = 0, visit = 0;
-            uint32_t phase = 0;
-            for (int k = k0; k < k1; ++k) {
-                const int u = k / nc, c = k - u * nc, jt = k - k0;
-                const int vb = visit & 1;
-                if (k == k0 || c == 0) {
-                    tc::mbar_wait(&v_full[vb], (visit >> 1) & 1);
-                    tc::fence_after_sync();
-                }
-                const int s = bl.site(c);
-                const uint32_t vhi = sbase + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES, vlo = vhi + L::V_BYTES;
-                tc::mbar_wait(&full[stage], phase);
-                const int db = jt & 1;
-                tc::mbar_wait(&d_empty[db], ((jt >> 1) & 1) ^ 1u);
-                tc::fence_after_sync();
-                if (a.prof && blockIdx.x == 0 && jt < 128) a.prof[512 + jt * 4 + 1] = clock64();
-                const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE + L::Y_BYTES;
-                const uint32_t dD = tmem + db * kSpNMax;
-                const uint32_t id = bl.cw[s] == kSpNMax ? id256 : id128;
-#pragma unroll
-                for (int kk = 0; kk < R / 16; ++kk) {
-                    const uint64_t bd = tc::desc_kmajor(bt + kk * 256, 128, R * 16);
-                    tc::mma_bf16(dD, tc::desc_kmajor(vhi + kk * 256, 128, R * 16), bd, id, kk > 0 ? 1u : 0u);
-                    tc::mma_bf16(dD, tc::desc_kmajor(vlo + kk * 256, 128, R * 16), bd, id, 1u);
-                }
-                tc::mma_commit(&d_full[db]);
-                tc::mma_commit(&empty[stage]);
-                if (++stage == L::STAGES) {
-                    stage = 0;
-                    phase ^= 1u;
-                }
-                // the unit's V buffer is free once its last item has been issued
-                if (k + 1 == k1 || c + 1 == nc) {
-                    tc::mma_commit(&v_empty[vb]);
-                    ++visit;
-                }
-            }
-        }
-    } else if (warp < 4) {
-        // P rows -> V = scale * P (bf16 hi + lo), 32 rows per warp, once per unit visit
-        int visit = 0;
-        for (int k = k0; k < k1; ++k) {
-            const int u = k / nc;
-            if (!(k == k0 || k == u * nc)) continue;
-            const int4 U = a.units[u];
-            const int vb = visit & 1;
-            const int m = (warp - 2) * 32 + lane, q = m >> 4, rr = m & 15;
-            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-            const bool valid = rr < ch.y;
-            const float* pr = static_cast<const float*>(a.P) + static_cast<long long>(ch.x + rr) * a.ldp;
-            tc::mbar_wait(&v_empty[vb], ((visit >> 1) & 1) ^ 1u);
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                const float sc = __ldg(static_cast<const float*>(a.site[s].scale) + U.x);
-                unsigned char* vhi = sgen + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES;
-#pragma unroll
-                for (int k0v = 0; k0v < R; k0v += 8) {
-                    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
-                    if (valid) {
-                        p0 = *reinterpret_cast<const float4*>(pr + s * R + k0v);
-                        p1 = *reinterpret_cast<const float4*>(pr + s * R + k0v + 4);
-                    }
-                    const float v[8] = {p0.x * sc, p0.y * sc, p0.z * sc, p0.w * sc,
-                                        p1.x * sc, p1.y * sc, p1.z * sc, p1.w * sc};
-                    uint32_t hi[4], lo[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        hi[e] = f32x2_to_bf16(v[2 * e], v[2 * e + 1]);
-                        float h0, h1;
-                        bf16x2_to_acc(hi[e], h0, h1);
-                        lo[e] = f32x2_to_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
-                    }
-                    const uint32_t off = tc::kmajor_offset(m, k0v, R);
-                    *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                    *reinterpret_cast<uint4*>(vhi + L::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                }
-            }
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&v_full[vb]);
-            ++visit;
-        }
-    } else {
-        // epilogue group g takes items k0 + g, k0 + g + 2, ...: D -> registers,
-        // y block += D in shared memory, TMA store (one 3D box per full chunk)
-        const int q = warp & 3, g = (warp - 4) >> 2;
-        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-        const uint64_t stream = tc::policy_evict_first();
-        const int r1 = lane >> 2, cp = 2 * (lane & 3);
-        int pu = -1;
-        int2 ch = make_int2(0, 0);
-        for (int k = k0 + g; k < k1; k += 2) {
-            const int u = k / nc, c = k - u * nc, jt = k - k0;
-            if (u != pu) {
-                const int4 U = a.units[u];
-                ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-                pu = u;
-            }
-            const int s = bl.site(c), j = c - bl.first[s], cw = bl.cw[s], npan = cw / 64;
-            const int stage = jt % L::STAGES;
-            const uint32_t phase = static_cast<uint32_t>(jt / L::STAGES) & 1u;
-            tc::mbar_wait(&d_full[g], (jt >> 1) & 1);
-            if (EPI == kEpiRmw) tc::mbar_wait(&full[stage], phase);
-            tc::fence_after_sync();
-            if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128)
-                a.prof[512 + jt * 4 + 2] = clock64();
-            if constexpr (EPI == kEpiReduce) {
-                // staging buffer (group g, item parity), this chunk's [panel][16][128 B]
-                const int sb = (jt >> 1) & 1;
-                const uint32_t tile = L::OFF_STG + ((g * 2 + sb) * 4 + q) * L::QS;
-                if (lane == 0) tc::tma_store_wait_read_1();  // this buffer's reduce of 2 items ago has read it
-                __syncwarp();
-                if (ch.y > 0) {
-                    for (int pass = 0; pass < npan / 2; ++pass) {
-                        uint32_t v[2][32];
-                        tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128, v[0]);
-                        tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128 + 64, v[1]);
-                        tc::tmem_ld_wait();
-#pragma unroll
-                        for (int pw = 0; pw < 2; ++pw) {
-                            const uint32_t panel = tile + (2 * pass + pw) * (kSpChunk * 128);
-#pragma unroll
-                            for (int i = 0; i < 8; ++i)
-#pragma unroll
-                                for (int half = 0; half < 2; ++half) {
-                                    const int r = r1 + 8 * half;
-                                    const uint32_t w = r < ch.y ? f32x2_to_bf16(__uint_as_float(v[pw][4 * i + 2 * half]),
-                                                                                 __uint_as_float(v[pw][4 * i + 2 * half + 1]))
-                                                                : 0x80008000u;  // -0.0: y + (-0) == y bit for bit
-                                    *reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(r, 8 * i + cp, kSpChunk)) = w;
-                                }
-                        }
-                    }
-                }
-                tc::fence_before_sync();
-                __syncwarp();
-                if (lane == 0) tc::mbar_arrive(&d_empty[g]);
-                if (ch.y > 0) {
-                    tc::fence_proxy_async();
-                    __syncwarp();
-                    if (lane == 0) {
-                        if (a.flags & kSplitHints)
-                            tc::tma_reduce_add_3d_hint(&maps.y[s], 0, ch.x, j * npan, sbase + tile, stream);
-                        else
-                            tc::tma_reduce_add_3d(&maps.y[s], 0, ch.x, j * npan, sbase + tile);
-                    }
-                }
-                if (lane == 0) {
-                    tc::tma_store_commit();
-                    if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && jt < 128) a.prof[512 + jt * 4 + 3] = clock64();
-                }
-                __syncwarp();
-                continue;
-            }
-            const uint32_t tile = L::OFF_RING + stage * L::STAGE + q * L::QS;  // this chunk's [panel][16][128 B]
-            if (ch.y > 0) {
-                for (int pass = 0; pass < npan / 2; ++pass) {
-                    uint32_t v[2][32];
-                    // loads, wait and every use of v stay in one block: a
-                    // tcgen05.ld whose registers are live across a branch join
-                    // can have them copied before tcgen05.wait::ld (stale D)
-                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128, v[0]);
-                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128 + 64, v[1]);
-                    tc::tmem_ld_wait();
-                    if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128 && pass == 0)
-                        a.prof[1024 + jt * 4 + 2] = clock64();
-#pragma unroll
-                    for (int pw = 0; pw < 2; ++pw) {
-                        const uint32_t panel = tile + (2 * pass + pw) * (kSpChunk * 128);
-                        uint32_t hv[16];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half)
-                                hv[2 * i + half] = *reinterpret_cast<const uint32_t*>(
-                                    sgen + panel + tc::sw128_offset(r1 + 8 * half, 8 * i + cp, kSpChunk));
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half) {
-                                float lo, hi;
-                                bf16x2_to_acc(hv[2 * i + half], lo, hi);
-                                lo += __uint_as_float(v[pw][4 * i + 2 * half]);
-                                hi += __uint_as_float(v[pw][4 * i + 2 * half + 1]);
-                                hv[2 * i + half] = f32x2_to_bf16(lo, hi);
-                            }
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half)
-                                *reinterpret_cast<uint32_t*>(
-                                    sgen + panel + tc::sw128_offset(r1 + 8 * half, 8 * i + cp, kSpChunk)) =
-                                    hv[2 * i + half];
-                    }
-                }
-            }
-            if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128)
-                a.prof[1024 + jt * 4 + 0] = clock64();
-            // D is free once read (warps without rows read nothing)
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&d_empty[g]);
-            if (ch.y > 0 && (a.flags & kSplitTmaStore)) {
-                tc::fence_proxy_async();
-                __syncwarp();
-                if (ch.y == kSpChunk && lane == 0) tc::tma_store_3d_hint(&maps.y[s], 0, ch.x, j * npan, sbase + tile, stream);
-            }
-            if (ch.y > 0 && (ch.y < kSpChunk || !(a.flags & kSplitTmaStore))) {
-                // rows straight from shared memory to global: 16 B per lane, a
-                // row's 256 or 128 columns per 32 or 16 lanes (coalesced), and
-                // only the chunk's own rows (past ch.y belong to other entries);
-                // the TMA engine then carries only the loads
-                __syncwarp();
-                __nv_bfloat16* yb = static_cast<__nv_bfloat16*>(a.site[s].y) + j * cw;
-                const long long ldy = a.site[s].ldy;
-                const int lg = cw == kSpNMax ? 5 : 4;  // log2(16 B vectors per row)
-                for (int idx = lane; idx < (ch.y << lg); idx += 32) {
-                    const int rr = idx >> lg, v16 = idx & ((1 << lg) - 1), pan = v16 >> 3, c16 = v16 & 7;
-                    const uint4 val = *reinterpret_cast<const uint4*>(
-                        sgen + tile + pan * (kSpChunk * 128) + tc::sw128_offset(rr, c16 * 8, kSpChunk));
-                    *reinterpret_cast<uint4*>(yb + static_cast<long long>(ch.x + rr) * ldy + pan * 64 + c16 * 8) = val;
-                }
-            }
-            if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && lane == 0 && jt < 128)
-                a.prof[1024 + jt * 4 + 1] = clock64();
-            __syncwarp();
-            if (lane == 0) {
-                // the stage is free once this item's stores have read shared
-                // memory (st.global: issued = read; TMA: wait for its reads)
-                if (a.flags & kSplitTmaStore) {
-                    tc::tma_store_commit();
-                    tc::tma_store_wait_read();
-                }
-                tc::mbar_arrive(&empty[stage]);
-                if (a.prof && blockIdx.x == 0 && warp == 4 + g * 4 && jt < 128) a.prof[512 + jt * 4 + 3] = clock64();
-            }
-            __syncwarp();
-        }
-        if (lane == 0) tc::tma_store_wait_all();
+    ExpandWork W{0, 0, a.sched, a.grab, 0};
+    if (!a.sched) {
+        CostModel cm;
+        cm.units = a.units;
+        cm.load(a.counters);
+        cm.alpha = kSpChunk * 4;          // y read + write per column per chunk
+        cm.beta = 2 * R + 16 + a.beta_e;  // Bt bytes per column + per-item overhead
+        cm.G = gridDim.x;
+        item_range(cm, bl, s_u, W.k0, W.k1);  // K1's output only: before the wait (see the shrink)
     }
-    tc::fence_before_sync();
-    __syncthreads();
-    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1793 + 2 * blockIdx.x] = tc::globaltimer();
-    if (warp == 0) {
-        __syncwarp();
-        tc::tmem_dealloc(tmem, 512);
-    }
-}
-// Dynamically scheduled expand (default with a workspace): the (unit, block)
-// items are handed out in grabs of a.grab consecutive items from a global
-// counter, so a CTA that meets slower memory simply takes fewer — the static
-// cost-balanced ranges finished at max/mean 1.29 across CTAs at config-4
-// shapes although every item ran at the SM's share of HBM (split_prof
-// timelines).  The producer grabs (one grab ahead, so the atomic's round trip
-// hides behind the current grab's loads) and posts each grab in a 4-slot
-// shared-memory queue that every other role walks in the same order; a
-// "visit" (one V build) is a run of items of one unit in that order.  The
-// last CTA out resets the counter for the next launch.
-//
-// warps: 0 grabs + Bt producer, 1 UMMA issuer, 2-3 P rows -> bf16 hi/lo V,
-//        4-7 / 8-11 epilogue groups (even / odd items of the CTA's sequence)
-template <int R, int NS>
-__global__ void __launch_bounds__(384, 1) expand_dyn_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
-    using L = ExpandLayout<R, NS, kEpiReduce>;
-    constexpr int Q = 4;
-    extern __shared__ unsigned char sm_raw[];
-    __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
-    __shared__ __align__(8) uint64_t v_full[2], v_empty[2], d_full[2], d_empty[2];
-    __shared__ __align__(8) uint64_t q_full[Q], q_empty[Q];
-    __shared__ int q_grab[Q];
-    __shared__ uint32_t tslot;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const uint32_t raw = tc::smem_u32(sm_raw);
-    const uint32_t sbase = (raw + 1023u) & ~1023u;
-    unsigned char* sgen = sm_raw + (sbase - raw);
-    if (warp == 0) tc::tmem_alloc(&tslot, 512);
-    if (tid == 32) {
-        for (int i = 0; i < L::STAGES; ++i) {
-            tc::mbar_init(&full[i], 1);
-            tc::mbar_init(&empty[i], 1);
-        }
-        for (int b = 0; b < 2; ++b) {
-            tc::mbar_init(&v_full[b], 2);
-            tc::mbar_init(&v_empty[b], 1);
-            tc::mbar_init(&d_full[b], 1);
-            tc::mbar_init(&d_empty[b], 4);
-        }
-        for (int i = 0; i < Q; ++i) {
-            tc::mbar_init(&q_full[i], 1);
-            tc::mbar_init(&q_empty[i], 1 + 2 + 8);  // every consumer warp (lane 0) once it has read the slot
-        }
-        tc::fence_mbar_init();
-    }
-    tc::fence_before_sync();
-    __syncthreads();
-    tc::fence_after_sync();
-    const uint32_t tmem = tslot;
-    tc::pdl_launch_dependents();
-    Blocks bl;
-    expand_blocks(bl, a, NS);
-    const int nc = bl.nc;
-    const int total = a.counters[PREFT_CTR_LORA_UNITS] * nc;
-    const int G = a.grab > 0 ? a.grab : 1;
-    const int ngrabs = (total + G - 1) / G;
+    W.total = a.counters[PREFT_CTR_LORA_UNITS] * bl.nc;
     tc::pdl_wait();  // P, y and the grab counter (reset by the previous launch) from here on
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1792 + 2 * blockIdx.x] = tc::globaltimer();
-
-    // walk the grab queue in order; body(k, jt) for every item k of the CTA's sequence
-    auto walk = [&](auto&& body) {
-        int qi = 0, jt = 0;
-        uint32_t qph = 0;
-        while (true) {
-            if (lane == 0) tc::mbar_wait(&q_full[qi], qph);
-            __syncwarp();
-            const int g = *reinterpret_cast<volatile int*>(&q_grab[qi]);
-            __syncwarp();
-            if (lane == 0 && g >= 0) tc::mbar_arrive(&q_empty[qi]);
-            if (g < 0) break;
-            const int kend = min(total, (g + 1) * G);
-            for (int k = g * G; k < kend; ++k) body(k, jt++);
-            if (++qi == Q) {
-                qi = 0;
-                qph ^= 1u;
-            }
-        }
-    };
-
-    if (warp == 0) {
-        if (lane == 0) {
-            const uint64_t keep = tc::policy_evict_last();
-            int stage = 0, qi = 0;
-            uint32_t phase = 0, qph = 0;
-            // the first grab is the CTA's own index (no atomic on the critical
-            // path at the start); later grabs come from the counter
-            int next = static_cast<int>(blockIdx.x);
-            while (true) {
-                const int cur = next;
-                const bool done = cur >= ngrabs;
-                if (!done) next = atomicAdd(a.sched, 1) + static_cast<int>(gridDim.x);  // consumed next iteration
-                tc::mbar_wait(&q_empty[qi], qph ^ 1u);
-                q_grab[qi] = done ? -1 : cur;
-                tc::mbar_arrive(&q_full[qi]);
-                if (++qi == Q) {
-                    qi = 0;
-                    qph ^= 1u;
-                }
-                if (done) break;
-                const int kend = min(total, (cur + 1) * G);
-                for (int k = cur * G; k < kend; ++k) {
-                    const int u = k / nc, c = k - u * nc;
-                    const int s = bl.site(c), j = c - bl.first[s], cw = bl.cw[s];
-                    const uint32_t bt_bytes = static_cast<uint32_t>(cw * R * 2);
-                    tc::mbar_wait(&empty[stage], phase ^ 1u);
-                    tc::mbar_expect_tx(&full[stage], bt_bytes);
-                    tc::bulk_load_1d_hint(sbase + L::OFF_RING + stage * L::STAGE,
-                                          static_cast<const unsigned char*>(a.site[s].Bt_tc) +
-                                              static_cast<long long>(a.units[u].x) * a.site[s].n * R * 2 +
-                                              static_cast<long long>(j) * bt_bytes,
-                                          bt_bytes, &full[stage], keep);
-                    if (++stage == L::STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        const uint32_t id128 = tc::idesc_bf16_f32(kSpU, kSpN), id256 = tc::idesc_bf16_f32(kSpU, kSpNMax);
-        int stage = 0, visit = -1, pu = -1;
-        uint32_t phase = 0;
-        walk([&](int k, int jt) {
-            if (lane != 0) return;
-            const int u = k / nc, c = k - u * nc;
-            if (u != pu) {
-                if (visit >= 0) tc::mma_commit(&v_empty[visit & 1]);  // covers the previous visit's UMMAs
-                ++visit;
-                pu = u;
-                tc::mbar_wait(&v_full[visit & 1], (visit >> 1) & 1);
-                tc::fence_after_sync();
-            }
-            const int vb = visit & 1, s = bl.site(c);
-            const uint32_t vhi = sbase + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES, vlo = vhi + L::V_BYTES;
-            tc::mbar_wait(&full[stage], phase);
-            const int db = jt & 1;
-            tc::mbar_wait(&d_empty[db], ((jt >> 1) & 1) ^ 1u);
-            tc::fence_after_sync();
-            const uint32_t bt = sbase + L::OFF_RING + stage * L::STAGE;
-            const uint32_t dD = tmem + db * kSpNMax;
-            const uint32_t id = bl.cw[s] == kSpNMax ? id256 : id128;
-#pragma unroll
-            for (int kk = 0; kk < R / 16; ++kk) {
-                const uint64_t bd = tc::desc_kmajor(bt + kk * 256, 128, R * 16);
-                tc::mma_bf16(dD, tc::desc_kmajor(vhi + kk * 256, 128, R * 16), bd, id, kk > 0 ? 1u : 0u);
-                tc::mma_bf16(dD, tc::desc_kmajor(vlo + kk * 256, 128, R * 16), bd, id, 1u);
-            }
-            tc::mma_commit(&d_full[db]);
-            tc::mma_commit(&empty[stage]);
-            if (++stage == L::STAGES) {
-                stage = 0;
-                phase ^= 1u;
-            }
-        });
-    } else if (warp < 4) {
-        int visit = -1, pu = -1;
-        walk([&](int k, int) {
-            const int u = k / nc;
-            if (u == pu) return;
-            pu = u;
-            ++visit;
-            const int4 U = a.units[u];
-            const int vb = visit & 1;
-            const int m = (warp - 2) * 32 + lane, q = m >> 4, rr = m & 15;
-            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-            const bool valid = rr < ch.y;
-            const float* pr = static_cast<const float*>(a.P) + static_cast<long long>(ch.x + rr) * a.ldp;
-            tc::mbar_wait(&v_empty[vb], ((visit >> 1) & 1) ^ 1u);
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                const float sc = __ldg(static_cast<const float*>(a.site[s].scale) + U.x);
-                unsigned char* vhi = sgen + L::OFF_V + ((vb * NS + s) * 2) * L::V_BYTES;
-#pragma unroll
-                for (int k0v = 0; k0v < R; k0v += 8) {
-                    float4 p0 = make_float4(0.f, 0.f, 0.f, 0.f), p1 = p0;
-                    if (valid) {
-                        p0 = *reinterpret_cast<const float4*>(pr + s * R + k0v);
-                        p1 = *reinterpret_cast<const float4*>(pr + s * R + k0v + 4);
-                    }
-                    const float v[8] = {p0.x * sc, p0.y * sc, p0.z * sc, p0.w * sc,
-                                        p1.x * sc, p1.y * sc, p1.z * sc, p1.w * sc};
-                    uint32_t hi[4], lo[4];
-#pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        hi[e] = f32x2_to_bf16(v[2 * e], v[2 * e + 1]);
-                        float h0, h1;
-                        bf16x2_to_acc(hi[e], h0, h1);
-                        lo[e] = f32x2_to_bf16(v[2 * e] - h0, v[2 * e + 1] - h1);
-                    }
-                    const uint32_t off = tc::kmajor_offset(m, k0v, R);
-                    *reinterpret_cast<uint4*>(vhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                    *reinterpret_cast<uint4*>(vhi + L::V_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-                }
-            }
-            tc::fence_proxy_async();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&v_full[vb]);
-        });
-    } else {
-        const int q = warp & 3, g = (warp - 4) >> 2;
-        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
-        const uint64_t stream = tc::policy_evict_first();
-        const int r1 = lane >> 2, cp = 2 * (lane & 3);
-        int pu = -1;
-        int2 ch = make_int2(0, 0);
-        walk([&](int k, int jt) {
-            if ((jt & 1) != g) return;
-            const int u = k / nc, c = k - u * nc;
-            if (u != pu) {
-                const int4 U = a.units[u];
-                ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
-                pu = u;
-            }
-            const int s = bl.site(c), j = c - bl.first[s], cw = bl.cw[s], npan = cw / 64;
-            tc::mbar_wait(&d_full[g], (jt >> 1) & 1);
-            tc::fence_after_sync();
-            const int sb = (jt >> 1) & 1;
-            const uint32_t tile = L::OFF_STG + ((g * 2 + sb) * 4 + q) * L::QS;
-            if (lane == 0) tc::tma_store_wait_read_1();
-            __syncwarp();
-            if (ch.y > 0) {
-                for (int pass = 0; pass < npan / 2; ++pass) {
-                    uint32_t v[2][32];
-                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128, v[0]);
-                    tc::tmem_ld_16x256b_x8(tmem + lane_base + g * kSpNMax + pass * 128 + 64, v[1]);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int pw = 0; pw < 2; ++pw) {
-                        const uint32_t panel = tile + (2 * pass + pw) * (kSpChunk * 128);
-#pragma unroll
-                        for (int i = 0; i < 8; ++i)
-#pragma unroll
-                            for (int half = 0; half < 2; ++half) {
-                                const int r = r1 + 8 * half;
-                                const uint32_t w = r < ch.y ? f32x2_to_bf16(__uint_as_float(v[pw][4 * i + 2 * half]),
-                                                                             __uint_as_float(v[pw][4 * i + 2 * half + 1]))
-                                                            : 0x80008000u;  // -0.0: y + (-0) == y bit for bit
-                                *reinterpret_cast<uint32_t*>(sgen + panel + tc::sw128_offset(r, 8 * i + cp, kSpChunk)) = w;
-                            }
-                    }
-                }
-            }
-            tc::fence_before_sync();
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&d_empty[g]);
-            if (ch.y > 0) {
-                tc::fence_proxy_async();
-                __syncwarp();
-                if (lane == 0) tc::tma_reduce_add_3d_hint(&maps.y[s], 0, ch.x, j * npan, sbase + tile, stream);
-            }
-            if (lane == 0) tc::tma_store_commit();
-            __syncwarp();
-        });
-        if (lane == 0) tc::tma_store_wait_all();
-    }
+    SplitVSrc vs{static_cast<const float*>(a.P), a.ldp};
+    expand_pipeline<R, NS>(maps, a, bl, sbase, sgen, tmem, B, W, vs);
     tc::fence_before_sync();
     __syncthreads();
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1793 + 2 * blockIdx.x] = tc::globaltimer();
-    if (tid == 0) {
-        // the last CTA out resets the grab counter for the next launch (every
-        // CTA's producer took its last grab before its CTA got here)
+    if (tid == 0 && a.sched) {
+        // the last CTA out resets the grab counter (every CTA's producer took
+        // its last grab before its CTA got here)
         __threadfence();
         if (atomicAdd(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
             a.sched[0] = 0;
@@ -1109,25 +552,14 @@ static int fill_common(SplitArgs& args, const preft_meta_t* meta, const preft_lo
     return PREFT_OK;
 }
 
-template <int EPI>
 static int launch_expand(const SplitMaps& maps, const SplitArgs& args, int nsites, int r, int num_sms, cudaStream_t stream) {
-    if (EPI == kEpiReduce && args.sched) {
-        if (r == 16) {
-            if (nsites == 1) return launch_tc(expand_dyn_kernel<16, 1>, ExpandLayout<16, 1, kEpiReduce>::SMEM, 384, maps, args, num_sms, stream);
-            if (nsites == 2) return launch_tc(expand_dyn_kernel<16, 2>, ExpandLayout<16, 2, kEpiReduce>::SMEM, 384, maps, args, num_sms, stream);
-            return launch_tc(expand_dyn_kernel<16, 3>, ExpandLayout<16, 3, kEpiReduce>::SMEM, 384, maps, args, num_sms, stream);
-        }
-        if (nsites == 1) return launch_tc(expand_dyn_kernel<32, 1>, ExpandLayout<32, 1, kEpiReduce>::SMEM, 384, maps, args, num_sms, stream);
-        if (nsites == 2) return launch_tc(expand_dyn_kernel<32, 2>, ExpandLayout<32, 2, kEpiReduce>::SMEM, 384, maps, args, num_sms, stream);
-        return PREFT_ERR_RANK;
-    }
     if (r == 16) {
-        if (nsites == 1) return launch_tc(expand_tc_kernel<16, 1, EPI>, ExpandLayout<16, 1, EPI>::SMEM, 384, maps, args, num_sms, stream);
-        if (nsites == 2) return launch_tc(expand_tc_kernel<16, 2, EPI>, ExpandLayout<16, 2, EPI>::SMEM, 384, maps, args, num_sms, stream);
-        return launch_tc(expand_tc_kernel<16, 3, EPI>, ExpandLayout<16, 3, EPI>::SMEM, 384, maps, args, num_sms, stream);
+        if (nsites == 1) return launch_tc(expand_tc_kernel<16, 1>, ExpandLayout<16, 1>::SMEM, 384, maps, args, num_sms, stream);
+        if (nsites == 2) return launch_tc(expand_tc_kernel<16, 2>, ExpandLayout<16, 2>::SMEM, 384, maps, args, num_sms, stream);
+        return launch_tc(expand_tc_kernel<16, 3>, ExpandLayout<16, 3>::SMEM, 384, maps, args, num_sms, stream);
     }
-    if (nsites == 1) return launch_tc(expand_tc_kernel<32, 1, EPI>, ExpandLayout<32, 1, EPI>::SMEM, 384, maps, args, num_sms, stream);
-    if (nsites == 2) return launch_tc(expand_tc_kernel<32, 2, EPI>, ExpandLayout<32, 2, EPI>::SMEM, 384, maps, args, num_sms, stream);
+    if (nsites == 1) return launch_tc(expand_tc_kernel<32, 1>, ExpandLayout<32, 1>::SMEM, 384, maps, args, num_sms, stream);
+    if (nsites == 2) return launch_tc(expand_tc_kernel<32, 2>, ExpandLayout<32, 2>::SMEM, 384, maps, args, num_sms, stream);
     return PREFT_ERR_RANK;
 }
 
@@ -1318,10 +750,8 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
         if (const char* e = getenv("PREFT_SPLIT_GRAB")) args.grab = atoi(e) > 0 ? atoi(e) : args.grab;
     }
     {
-        const char* env = getenv("PREFT_SPLIT_TMA_STORE");
-        args.flags = (env && env[0] == '1') ? kSplitTmaStore : 0;
         const char* h = getenv("PREFT_SPLIT_HINTS");  // default on (+0.3%, profiles/split_tuning_r02c.txt)
-        if (!(h && h[0] == '0')) args.flags |= kSplitHints;
+        args.flags = (h && h[0] == '0') ? 0 : kSplitHints;
     }
     const int variant = split_variant();
     const bool tc_ok = expand_tc_ok(meta, P, ldp, sites, nsites, r, dtype);
@@ -1335,9 +765,7 @@ int lora_expand(const preft_meta_t* meta, const void* P, long long ldp, long lon
                                        static_cast<unsigned long long>(sites[s].ldy), kSpChunk, npan))
                 return PREFT_ERR_CONFIG;
         }
-        const char* epi = getenv("PREFT_SPLIT_EPI");
-        if (epi && epi[0] == 'r' && epi[1] == 'm') return launch_expand<kEpiRmw>(maps, args, nsites, r, num_sms, stream);
-        return launch_expand<kEpiReduce>(maps, args, nsites, r, num_sms, stream);
+        return launch_expand(maps, args, nsites, r, num_sms, stream);
     }
     const int W = dtype == PREFT_DTYPE_BF16 ? 8 : dtype == PREFT_DTYPE_F32 ? 4 : 2;
     bool vec = true;

@@ -35,7 +35,7 @@ struct SplitArgs {
     float* planes;  // partial planes p >= 1 at planes + p * plane_stride (row stride ldp)
     long long plane_stride;
     int* sync;      // per-unit arrival counters (zero between launches)
-    int flags;      // kSplitTmaStore: the expand stores full chunks by TMA (default: st.global from smem)
+    int flags;      // kSplitHints
     int* sched;     // dynamic expand: [0] next grab, [1] finished CTAs (zero between launches); NULL = static ranges
     int grab;       // items per grab
     int beta_s;     // added to the shrink / expand cost models' per-column item overhead
@@ -63,9 +63,8 @@ constexpr int kPlanes = 4;                // max CTAs sharing one unit's shrink 
 // (12.1 -> 11.4-11.7 ms/step) and the 8B r16 step
 constexpr int kBetaS = 128;
 constexpr int kBetaE = 128;
-constexpr int kSplitTmaStore = 1;
-constexpr int kSplitHints = 2;
-constexpr int kSchedInts = 8;  // expand: Bt loads evict_last, y reduce-adds evict_first
+constexpr int kSplitHints = 2;  // expand: Bt loads evict_last, y reduce-adds evict_first
+constexpr int kSchedInts = 8;   // the dynamic expand's counters in meta->lora_part
 
 struct SplitMaps {
     CUtensorMap x;       // x [rows][m] (this rank's columns), 16-row x 64-col boxes
@@ -253,24 +252,20 @@ __device__ __forceinline__ void readout_bar() { asm volatile("bar.sync 1, 128;" 
 
 // ---- expand
 
-// EPI = kEpiRmw: y rows come into the ring by TMA, the epilogue adds D in
-// shared memory and stores the rows back.  EPI = kEpiReduce: the ring holds
-// only Bt; the epilogue writes bf16(D) into a staging tile and a TMA
-// reduce-add adds it into y in L2 (rows of a partial chunk beyond the
-// entry's own are padded with -0.0, which leaves any value and the sign of
-// zero unchanged), so y never passes through the SM.
-constexpr int kEpiRmw = 0, kEpiReduce = 1;
-
-template <int R, int NS, int EPI>
+// The expand's shared-memory layout: Bt blocks in a ring (TMA bulk copies),
+// the unit's V (hi / lo, double-buffered) and the epilogue's bf16 staging
+// tiles, from which a TMA reduce-add adds the delta into y in L2 (rows of a
+// partial chunk beyond the entry's own are padded with -0.0, which leaves any
+// value and the sign of zero unchanged), so y never passes through the SM.
+template <int R, int NS>
 struct ExpandLayout {
     static constexpr int QS = 4 * kSpChunk * 128;         // one chunk's rows of a block: <= 4 panels x 16 rows x 128 B
-    static constexpr int Y_BYTES = EPI == kEpiRmw ? 4 * QS : 0;  // the y rows of 4 chunks (32 KB)
     static constexpr int BT_BYTES = kSpNMax * R * 2;
-    static constexpr int STAGE = Y_BYTES + BT_BYTES;      // multiple of 1024
+    static constexpr int STAGE = BT_BYTES;                // multiple of 1024
     static constexpr int V_BYTES = kSpU * R * 2;          // one V (hi or lo) of one site
     static constexpr int OFF_V = 0;                       // [2 buffers][NS sites][hi, lo]
     static constexpr int OFF_STG = 4 * NS * V_BYTES;      // reduce staging [2 groups][2 buffers][4 chunks] x QS
-    static constexpr int STG_BYTES = EPI == kEpiReduce ? 2 * 2 * 4 * QS : 0;
+    static constexpr int STG_BYTES = 2 * 2 * 4 * QS;
     static constexpr int OFF_RING = OFF_STG + STG_BYTES;  // multiple of 1024
     static constexpr int STAGES_FIT = (227 * 1024 - 2048 - OFF_RING) / STAGE;
     static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
