@@ -294,3 +294,21 @@ def test_rank16_32_tensor_core_route(cuda_device, variant, rank):
                 assert torch.equal(y, w)
     finally:
         lib.preft_set_lora_variant(-1)
+
+
+def test_tensor_core_route_with_dynamic_grabs_forced():
+    """The dynamic expand (item grabs from a global counter) on every TC
+    launch, not only the wide groups it is chosen for: the r = 16/32 route's
+    parity and CUDA-graph checks rerun in a process with PREFT_SPLIT_DYN=1
+    (the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, PREFT_SPLIT_DYN="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        str(root / "tests" / "test_gpu_lora.py"), "-k", "rank16_32_tensor_core_route"],
+                       capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
