@@ -90,6 +90,7 @@ extern "C" {
 /* rows per chunk: one TMA box / one TMEM lane quadrant of an M = 64 UMMA */
 #define PREFT_CHUNK_ROWS 16
 #define PREFT_UNIT_CHUNKS 4
+#define PREFT_META_UNIT_ORDER 1
 
 /*
  * Batch-metadata workspace.  All arrays are device memory at fixed addresses
@@ -143,7 +144,10 @@ typedef struct preft_meta {
     int32_t* chunks;
     int32_t* units;
     int32_t chunk_cap;   /* >= E_cap + T_cap / PREFT_CHUNK_ROWS + 1 (bounds chunks and units) */
-    int32_t reserved;
+    int32_t meta_flags;  /* PREFT_META_UNIT_ORDER: units[] holds 5 * chunk_cap ints and K1 appends,
+                            at units + 4 * chunk_cap, the LoRA-class units in size order (4 chunks
+                            first, then 3, 2, 1; K1 order within a size) — the tensor-core shrink
+                            hands them out largest first */
     float* lora_part;    /* NULL, or a [T_cap][nsites * r_max] f32 workspace for the rank-r
                             intermediate of tensor-core LoRA launches (bf16, r_max 16/32) */
     int64_t lora_part_floats; /* capacity of lora_part in floats */

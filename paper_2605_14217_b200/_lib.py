@@ -44,6 +44,7 @@ CTR_LORA_CHUNKS = 11
 NUM_COUNTERS = 12
 CHUNK_ROWS = 16
 UNIT_CHUNKS = 4
+META_UNIT_ORDER = 1
 SLOT_SPLIT_ALL_LORA = 2**31 - 1  # every slot is a LoRA-class slot
 MAX_ENTRIES = 4096
 
@@ -68,7 +69,7 @@ class PreftMeta(ctypes.Structure):
         ("chunks", ctypes.c_void_p),
         ("units", ctypes.c_void_p),
         ("chunk_cap", ctypes.c_int32),
-        ("reserved", ctypes.c_int32),
+        ("meta_flags", ctypes.c_int32),
         ("lora_part", ctypes.c_void_p),
         ("lora_part_floats", ctypes.c_int64),
     ]

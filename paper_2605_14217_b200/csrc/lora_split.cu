@@ -411,6 +411,241 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
 }
 
 
+// LPT shrink (opt-in, PREFT_SPLIT_LPT=1; needs K1's size order): whole units
+// handed out largest first — the CTA's own index first, then from a global
+// counter one grab ahead — through a 4-slot shared-memory queue that every
+// role walks.  At ~1.6 units per CTA the cost-balanced contiguous ranges
+// left the slowest CTA at ~1.7x the mean (whole units cannot be split
+// without summing partials, which costs more than it saves); greedy
+// largest-first brings it to ~1.2x.  The last CTA out resets the counter.
+//
+// warps: 0 grabs + TMA producer (x), 6 TMA producer (A), 1 + 7..9 UMMA
+// issuers, 2..5 TMEM -> P rows (lane quadrant = warp % 4)
+template <int R, int NS>
+__global__ void __launch_bounds__(kShrinkThreads, 1) shrink_lpt_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
+    using L = ShrinkLayout<R, NS>;
+    constexpr int Q = 4, CONSUMERS = 1 + kSpAcc + 4;
+    extern __shared__ unsigned char sm_raw[];
+    __shared__ __align__(8) uint64_t full[L::STAGES], empty[L::STAGES];
+    __shared__ __align__(8) uint64_t s_full[2], s_empty[2];
+    __shared__ __align__(8) uint64_t q_full[Q], q_empty[Q];
+    __shared__ int q_u[Q];
+    __shared__ uint32_t tslot;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t sbase = (tc::smem_u32(sm_raw) + 1023u) & ~1023u;
+    if (warp == 0) tc::tmem_alloc(&tslot, L::TMEM_COLS);
+    if (tid == 32) {
+        for (int i = 0; i < L::STAGES; ++i) {
+            tc::mbar_init(&full[i], 1);
+            tc::mbar_init(&empty[i], kSpAcc);
+        }
+        for (int b = 0; b < 2; ++b) {
+            tc::mbar_init(&s_full[b], kSpAcc);
+            tc::mbar_init(&s_empty[b], 4);
+        }
+        for (int i = 0; i < Q; ++i) {
+            tc::mbar_init(&q_full[i], 1);
+            tc::mbar_init(&q_empty[i], CONSUMERS);
+        }
+        tc::fence_mbar_init();
+        tc::prefetch_tmap(&maps.x);
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+    const uint32_t tmem = tslot;
+    tc::pdl_launch_dependents();
+    const int nlu = a.counters[PREFT_CTR_LORA_UNITS];
+    const int* order = a.unit_order;
+    // K1's output: the first grab is known before the wait
+    int first_u = -1;
+    if (warp == 0 && lane == 0 && static_cast<int>(blockIdx.x) < nlu) first_u = order[blockIdx.x];
+    tc::pdl_wait();  // x, A, P and the grab counter (reset by the previous launch) from here on
+    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1536 + 2 * blockIdx.x] = tc::globaltimer();
+    const int np = a.m / 64;
+    int* ctr = a.sched + 2;
+
+    // consumers: every posted unit in order
+    auto walk = [&](auto&& body) {
+        int qi = 0;
+        uint32_t qph = 0;
+        while (true) {
+            if (lane == 0) tc::mbar_wait(&q_full[qi], qph);
+            __syncwarp();
+            const int u = *reinterpret_cast<volatile int*>(&q_u[qi]);
+            __syncwarp();
+            if (u < 0) break;
+            if (lane == 0) tc::mbar_arrive(&q_empty[qi]);
+            body(u);
+            if (++qi == Q) {
+                qi = 0;
+                qph ^= 1u;
+            }
+        }
+    };
+
+    if (warp == 0) {
+        const uint64_t stream = tc::policy_evict_first();
+        int stage = 0, qi = 0;
+        uint32_t phase = 0, qph = 0;
+        int cur_u = first_u;      // lane 0
+        int next_g = -1;          // lane 0: the next grab index, in flight
+        if (lane == 0 && cur_u >= 0) next_g = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
+        while (true) {
+            if (lane == 0) {
+                tc::mbar_wait(&q_empty[qi], qph ^ 1u);
+                q_u[qi] = cur_u;
+                tc::mbar_arrive(&q_full[qi]);
+            }
+            const int u = __shfl_sync(0xffffffffu, cur_u, 0);
+            if (++qi == Q) {
+                qi = 0;
+                qph ^= 1u;
+            }
+            if (u < 0) break;
+            // the next unit: its order[] load and the grab after it go out now,
+            // their round trips overlap this unit's loads
+            int nu_ = -1;
+            if (lane == 0) {
+                if (next_g < nlu) {
+                    nu_ = order[next_g];
+                    next_g = atomicAdd(ctr, 1) + static_cast<int>(gridDim.x);
+                }
+            }
+            const int4 U = a.units[u];
+            const int n = U.z;
+            const int row = lane < n ? a.chunks[U.y + lane].x : 0;
+            const int r0 = __shfl_sync(0xffffffffu, row, 0);
+            const bool contig = unit_contiguous(a.chunks, U);
+            const uint32_t bytes = static_cast<uint32_t>(kPps * (n * kSpChunk * 128 + NS * L::AP_BYTES));
+            const int rq = __shfl_sync(0xffffffffu, row, lane & 3);
+            for (int p = 0; p < np; p += kPps) {
+                if (lane == 0) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1u);
+                    tc::mbar_expect_tx(&full[stage], bytes);
+                }
+                __syncwarp();
+                const uint32_t st = sbase + stage * L::STAGE;
+                if (contig) {
+                    if (lane < kPps)
+                        tc::tma_load_2d_hint(st + lane * L::PANEL, &maps.x64, (p + lane) * 64, r0, &full[stage], stream);
+                } else if (lane < 4 * kPps) {
+                    const int pp = lane >> 2, q = lane & 3;
+                    if (q < n)
+                        tc::tma_load_2d_hint(st + pp * L::PANEL + q * (kSpChunk * 128), &maps.x, (p + pp) * 64, rq,
+                                             &full[stage], stream);
+                }
+                if (++stage == L::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+            cur_u = nu_;
+        }
+    } else if (warp == 6) {
+        int stage = 0;
+        uint32_t phase = 0;
+        walk([&](int u) {
+            if (lane != 0) return;
+            const int slot = a.units[u].x;
+            for (int p = 0; p < np; p += kPps) {
+                tc::mbar_wait(&empty[stage], phase ^ 1u);
+                const uint32_t st = sbase + stage * L::STAGE;
+#pragma unroll
+                for (int pp = 0; pp < kPps; ++pp)
+#pragma unroll
+                    for (int s = 0; s < NS; ++s)
+                        tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s], (p + pp) * 64,
+                                        slot * R, &full[stage]);
+                if (++stage == L::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+        });
+    } else if (warp == 1 || warp >= 7) {
+        const int mw = warp == 1 ? 0 : warp - 6;
+        const uint32_t id = tc::idesc_bf16_f32(kSpU, L::NSR);
+        int stage = 0, ub = 0;
+        uint32_t phase = 0;
+        walk([&](int) {
+            if (lane != 0) return;
+            const int sb = ub & 1;
+            const uint32_t dS = tmem + sb * kSpAcc * L::NSR;
+            tc::mbar_wait(&s_empty[sb], ((ub >> 1) & 1) ^ 1u);
+            tc::fence_after_sync();
+            for (int p = 0; p < np; p += kPps) {
+                tc::mbar_wait(&full[stage], phase);
+                tc::fence_after_sync();
+                const uint32_t st = sbase + stage * L::STAGE;
+#pragma unroll
+                for (int j = mw; j < 4 * kPps; j += kSpAcc) {
+                    const int pp = j >> 2, kq = j & 3;
+                    tc::mma_bf16(dS + mw * L::NSR, tc::desc_kmajor_sw128(st + pp * L::PANEL + kq * 32),
+                                 tc::desc_kmajor_sw128(st + L::X_BYTES + pp * NS * L::AP_BYTES + kq * 32), id,
+                                 p * 4 + j >= kSpAcc ? 1u : 0u);
+                }
+                tc::mma_commit(&empty[stage]);
+                if (++stage == L::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
+            }
+            tc::mma_commit(&s_full[sb]);
+            ++ub;
+        });
+    } else if (warp < 6) {
+        const int q = warp & 3;
+        const uint32_t lane_base = static_cast<uint32_t>(q * 32) << 16;
+        int ub = 0;
+        walk([&](int u) {
+            const int4 U = a.units[u];
+            const int2 ch = q < U.z ? a.chunks[U.y + q] : make_int2(0, 0);
+            const int sb = ub & 1;
+            tc::mbar_wait(&s_full[sb], (ub >> 1) & 1);
+            tc::fence_after_sync();
+            float s[L::NSR];
+#pragma unroll
+            for (int c = 0; c < L::NSR; ++c) s[c] = 0.f;
+#pragma unroll
+            for (int acc = 0; acc < kSpAcc; ++acc)
+#pragma unroll
+                for (int cc = 0; cc < L::NSR; cc += 16) {
+                    uint32_t w[16];
+                    tc::tmem_ld16(tmem + lane_base + sb * kSpAcc * L::NSR + acc * L::NSR + cc, w);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) s[cc + c] += __uint_as_float(w[c]);
+                }
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&s_empty[sb]);
+            if (lane < ch.y) {
+                float* pr = static_cast<float*>(a.P) + static_cast<long long>(ch.x + lane) * a.ldp;
+#pragma unroll
+                for (int c = 0; c < L::NSR; c += 4)
+                    *reinterpret_cast<float4*>(pr + c) = make_float4(s[c], s[c + 1], s[c + 2], s[c + 3]);
+            }
+            ++ub;
+        });
+    }
+    tc::fence_before_sync();
+    __syncthreads();
+    if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1537 + 2 * blockIdx.x] = tc::globaltimer();
+    if (tid == 0) {
+        __threadfence();
+        if (atomicAdd(a.sched + 3, 1) == static_cast<int>(gridDim.x) - 1) {
+            a.sched[2] = 0;
+            a.sched[3] = 0;
+            __threadfence();
+        }
+    }
+    if (warp == 0) {
+        __syncwarp();
+        tc::tmem_dealloc(tmem, L::TMEM_COLS);
+    }
+}
+
 // The expand (the pipeline in expand.cuh): static cost-balanced item ranges,
 // or dynamic grabs (a.sched) for wide groups — the static ranges finished at
 // max/mean 1.29 across CTAs at config-4 gate/up although every item ran at
@@ -699,6 +934,27 @@ int lora_shrink(const preft_meta_t* meta, const void* x, long long rows, long lo
         split_planes(args, meta);
         args.prof = g_split_prof;
         split_tuning(args);
+        // largest-first whole units from K1's size order: opt-in (PREFT_SPLIT_LPT=1).
+        // Measured (profiles/split_tuning_r02c.txt): 8B r16 shrink 4.88 -> 4.61 ms/step,
+        // but config 4 4.18 -> 4.46 — the size order separates units of one adapter,
+        // whose A panels then come from DRAM twice instead of once plus L2
+        static int lpt = -1;
+        if (lpt < 0) {
+            const char* e = getenv("PREFT_SPLIT_LPT");
+            lpt = (e && e[0] == '1') ? 1 : 0;
+        }
+        args.sched = split_sched(meta);
+        args.unit_order = meta->units + 4 * static_cast<long long>(meta->chunk_cap);
+        if (lpt && args.max_planes <= 1 && args.sched && (meta->meta_flags & PREFT_META_UNIT_ORDER)) {
+            if (r == 16) {
+                if (nsites == 1) return launch_tc(shrink_lpt_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+                if (nsites == 2) return launch_tc(shrink_lpt_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+                return launch_tc(shrink_lpt_kernel<16, 3>, ShrinkLayout<16, 3>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+            }
+            if (nsites == 1) return launch_tc(shrink_lpt_kernel<32, 1>, ShrinkLayout<32, 1>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+            if (nsites == 2) return launch_tc(shrink_lpt_kernel<32, 2>, ShrinkLayout<32, 2>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
+            return PREFT_ERR_RANK;
+        }
         if (r == 16) {
             if (nsites == 1) return launch_tc(shrink_tc_kernel<16, 1>, ShrinkLayout<16, 1>::SMEM, kShrinkThreads, maps, args, num_sms, stream);
             if (nsites == 2) return launch_tc(shrink_tc_kernel<16, 2>, ShrinkLayout<16, 2>::SMEM, kShrinkThreads, maps, args, num_sms, stream);

@@ -290,6 +290,28 @@ __global__ void __launch_bounds__(kSortThreads, 1) meta_sort_kernel(const preft_
             reinterpret_cast<int4*>(m.units)[j] =
                 make_int4(m.segments[3 * s + 0], first, min(PREFT_UNIT_CHUNKS, end - first), 0);
         }
+        // the LoRA-class units in size order (4 chunks first, ..., 1 last; K1 order
+        // within a size) for the largest-first (LPT) tensor-core shrink: at ~1.6
+        // units per CTA it brings the slowest CTA's share from ~1.7x to ~1.2x the
+        // mean in a cost simulation (profiles/split_tuning_r02c.txt has the
+        // measurement, where adapter locality costs most of that back)
+        if (m.meta_flags & PREFT_META_UNIT_ORDER) {
+            __syncthreads();
+            int* order = m.units + 4 * m.chunk_cap;
+            const int nlu = s_lora_units;
+            const int per = (nlu + blockDim.x - 1) / blockDim.x;
+            const int beg = min(nlu, tid * per), end = min(nlu, beg + per);
+            int base = 0;
+            for (int z = PREFT_UNIT_CHUNKS; z >= 1; --z) {
+                int local = 0;
+                for (int j = beg; j < end; ++j) local += reinterpret_cast<const int4*>(m.units)[j].z == z;
+                int run = base + block_exclusive_sum(local, s_warp, &s_total);
+                for (int j = beg; j < end; ++j)
+                    if (reinterpret_cast<const int4*>(m.units)[j].z == z) order[run++] = j;
+                base += s_total;
+                __syncthreads();  // s_total is rewritten by the next scan
+            }
+        }
     } else {
         err |= PREFT_META_ERR_UNITS;
     }

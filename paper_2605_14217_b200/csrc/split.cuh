@@ -36,7 +36,9 @@ struct SplitArgs {
     long long plane_stride;
     int* sync;      // per-unit arrival counters (zero between launches)
     int flags;      // kSplitHints
-    int* sched;     // dynamic expand: [0] next grab, [1] finished CTAs (zero between launches); NULL = static ranges
+    int* sched;     // dynamic schedules (zero between launches): expand [0] next grab, [1] finished CTAs;
+                    //   LPT shrink [2], [3]; NULL = static ranges
+    const int* unit_order;  // K1's size order of the LoRA units (PREFT_META_UNIT_ORDER)
     int grab;       // items per grab
     int beta_s;     // added to the shrink / expand cost models' per-column item overhead
     int beta_e;     //   (tuning; env PREFT_SPLIT_BETA_S / _E)

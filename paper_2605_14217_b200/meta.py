@@ -96,7 +96,8 @@ class BatchMeta:
         self.tiles = torch.zeros(4 * self.tile_cap, **i32)
         self.entry_offset = torch.zeros(self.E_cap, **i32)
         self.chunks = torch.zeros(2 * self.chunk_cap, **i32)
-        self.units = torch.zeros(4 * self.chunk_cap, **i32)
+        # 4 ints per unit + the LoRA units' size order that K1 appends (PREFT_META_UNIT_ORDER)
+        self.units = torch.zeros(5 * self.chunk_cap, **i32)
         self.counters = torch.zeros(_lib.NUM_COUNTERS, **i32)
         self.host = torch.zeros(words, dtype=torch.int32, pin_memory=True)
         self._host_np = self.host.numpy()
@@ -118,7 +119,7 @@ class BatchMeta:
             self.chunks.data_ptr(),
             self.units.data_ptr(),
             self.chunk_cap,
-            0,
+            _lib.META_UNIT_ORDER,
             None,
             0,
         )
@@ -254,6 +255,11 @@ class BatchMeta:
     def chunks_host(self) -> np.ndarray:
         n = int(self.counters_host()[_lib.CTR_CHUNKS])
         return self.chunks[: 2 * n].view(n, 2).cpu().numpy()
+
+    def unit_order_host(self) -> np.ndarray:
+        """The LoRA-class units in size order (largest first), as K1 appends them."""
+        n = int(self.counters_host()[_lib.CTR_LORA_UNITS])
+        return self.units[4 * self.chunk_cap: 4 * self.chunk_cap + n].cpu().numpy()
 
     def units_host(self) -> np.ndarray:
         n = int(self.counters_host()[_lib.CTR_UNITS])

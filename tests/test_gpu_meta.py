@@ -43,6 +43,10 @@ def _check_meta(meta, qsl, slots, flags, tile_tokens, split):
     assert (u_slot[:n_lora] < split).all() and (u_slot[n_lora:] >= split).all()
     u_nch = np.asarray(units).reshape(-1, 4)[:, 2]
     assert int(c[_lib.CTR_LORA_CHUNKS]) == int(u_nch[:n_lora].sum())
+    # the LoRA units' size order K1 appends (PREFT_META_UNIT_ORDER): 4 chunks first, then
+    # 3, 2, 1, unit order within a size — a stable sort by decreasing chunk count
+    order = meta.unit_order_host()
+    assert np.array_equal(order, np.argsort(-u_nch[:n_lora], kind="stable"))
 
 
 def test_masks_and_grouping_on_golden_batches(cuda_device):
