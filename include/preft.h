@@ -244,7 +244,9 @@ int64_t preft_lora_part_floats(const preft_meta_t* meta);
  *   part [2 parities][tp src][planes][T_cap][64] f32 — src's partial P rows
  *   flag [2 parities][tp src][planes][U_cap] int32 — tag of the launch that
  *                                                      wrote them
- *   state [4] int32 — launch count, finished CTAs, error bits
+ *   state int32 — [2] error bits; from [16] the launch-sequence counters
+ *        (each CTA's launch count, which numbers the launch and is its tag;
+ *        the grid must therefore stay the same on an exchange)
  * A CTA that finishes a unit's shrink piece stores its partial rows into
  * every rank's region (P2P stores over NVLink) and then the piece's flag
  * (system-scope release); the expand of that unit waits for all tp x pieces

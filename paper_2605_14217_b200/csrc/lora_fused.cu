@@ -51,7 +51,7 @@ struct XchgArgs {
     long long spin_ns;
     int beta_s, beta_e;  // cost-model tuning (env PREFT_FUSED_BETA_S / _E)
     int knobs;           // experiments: bit 0 no producer fence
-    int dyn, grab;       // phase 2: dynamic item grabs (state[3] is the counter), items per grab
+    int dyn, grab;       // phase 2: dynamic item grabs (LaunchSeq at state + 16), items per grab
 };
 
 
@@ -165,7 +165,6 @@ __global__ void __launch_bounds__(384, 1)
     __shared__ int q_lo[kExpQ], q_hi[kExpQ];
     __shared__ uint32_t tslot;
     __shared__ int s_u[2];
-    __shared__ int s_tag;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const uint32_t raw = tc::smem_u32(sm_raw);
     const uint32_t sbase = (raw + 1023u) & ~1023u;
@@ -212,9 +211,11 @@ __global__ void __launch_bounds__(384, 1)
     const int ncs = bs.nc, nce = be.nc;
 
     tc::pdl_wait();
-    if (tid == 0) s_tag = *reinterpret_cast<volatile int*>(xa.state) + 1;
-    __syncthreads();
-    const int tag = s_tag, par = tag & 1;
+    // the launch's tag: every CTA's own launch count + 1 (LaunchSeq, split.cuh) —
+    // the same on every CTA and, with the same launch sequence, on every rank
+    int* seqb = xa.state + 16;
+    const LaunchSeq seq = launch_seq_begin(seqb);
+    const int tag = seq.n + 1, par = tag & 1;
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1536 + 2 * blockIdx.x] = tc::globaltimer();
 
     // ================================================================ phase 1: shrink
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(384, 1)
 
     // ================================================================ phase 2: expand
     {
-        ExpandWork W{e0, e1, xa.dyn ? xa.state + 3 : nullptr, xa.grab, a.counters[PREFT_CTR_LORA_UNITS] * nce};
+        ExpandWork W{e0, e1, xa.dyn ? seq.grab : nullptr, xa.grab, a.counters[PREFT_CTR_LORA_UNITS] * nce};
         XchgVSrc vs{xa.part[xa.rank], xa.flag[xa.rank], xa.state, &cs, &bs, xa.tp, xa.planes, xa.T_cap, xa.U_cap,
                     par, tag, sys, xa.spin_ns, 1};
         expand_pipeline<R, NS>(maps, a, be, sbase, sgen, tmem, EB, W, vs);
@@ -393,17 +394,7 @@ __global__ void __launch_bounds__(384, 1)
     tc::fence_before_sync();
     __syncthreads();
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1280 + blockIdx.x] = tc::globaltimer();
-    if (tid == 0) {
-        // the last CTA out advances the launch count (the next launch's tag);
-        // every CTA read it before any CTA could get here
-        __threadfence();
-        if (atomicAdd(xa.state + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-            xa.state[1] = 0;
-            xa.state[3] = 0;  // phase 2's grab counter
-            __threadfence();
-            atomicExch(xa.state, tag);
-        }
-    }
+    if (tid == 0) launch_seq_end(seqb, seq.n);
     if (warp == 0) {
         __syncwarp();
         tc::tmem_dealloc(tmem, 512);
@@ -416,7 +407,7 @@ bool pdl_enabled();
 long long* split_profile_buffer();
 
 long long xchg_region_bytes(int tp, int planes, int T_cap, int U_cap) {
-    return 2ll * tp * planes * T_cap * 64 * 4 + 2ll * tp * planes * U_cap * 4 + 64;
+    return 2ll * tp * planes * T_cap * 64 * 4 + 2ll * tp * planes * U_cap * 4 + (16 + kSeqInts) * 4;
 }
 
 int xchg_init(preft_xchg_t* xg, void* const* bases, int tp, int rank, int planes, int T_cap, int U_cap, int peer_sys) {

@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
 // role walks.  At ~1.6 units per CTA the cost-balanced contiguous ranges
 // left the slowest CTA at ~1.7x the mean (whole units cannot be split
 // without summing partials, which costs more than it saves); greedy
-// largest-first brings it to ~1.2x.  The last CTA out resets the counter.
+// largest-first brings it to ~1.2x.  Grab counters: LaunchSeq (split.cuh).
 //
 // warps: 0 grabs + TMA producer (x), 6 TMA producer (A), 1 + 7..9 UMMA
 // issuers, 2..5 TMEM -> P rows (lane quadrant = warp % 4)
@@ -460,10 +460,12 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_lpt_kernel(const __g
     // K1's output: the first grab is known before the wait
     int first_u = -1;
     if (warp == 0 && lane == 0 && static_cast<int>(blockIdx.x) < nlu) first_u = order[blockIdx.x];
-    tc::pdl_wait();  // x, A, P and the grab counter (reset by the previous launch) from here on
+    tc::pdl_wait();  // x, A, P and the launch-sequence counters from here on
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1536 + 2 * blockIdx.x] = tc::globaltimer();
     const int np = a.m / 64;
-    int* ctr = a.sched + 2;
+    int* seqb = a.sched + kSeqInts;
+    const LaunchSeq seq = launch_seq_begin(seqb);
+    int* ctr = seq.grab;
 
     // consumers: every posted unit in order
     auto walk = [&](auto&& body) {
@@ -632,14 +634,7 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_lpt_kernel(const __g
     tc::fence_before_sync();
     __syncthreads();
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1537 + 2 * blockIdx.x] = tc::globaltimer();
-    if (tid == 0) {
-        __threadfence();
-        if (atomicAdd(a.sched + 3, 1) == static_cast<int>(gridDim.x) - 1) {
-            a.sched[2] = 0;
-            a.sched[3] = 0;
-            __threadfence();
-        }
-    }
+    if (tid == 0) launch_seq_end(seqb, seq.n);
     if (warp == 0) {
         __syncwarp();
         tc::tmem_dealloc(tmem, L::TMEM_COLS);
@@ -649,7 +644,8 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_lpt_kernel(const __g
 // The expand (the pipeline in expand.cuh): static cost-balanced item ranges,
 // or dynamic grabs (a.sched) for wide groups — the static ranges finished at
 // max/mean 1.29 across CTAs at config-4 gate/up although every item ran at
-// the SM's share of HBM.  The last CTA out resets the grab counter.
+// the SM's share of HBM.  Grab counters come from the launch sequence
+// (split.cuh), so no CTA waits on an end-of-kernel handshake.
 template <int R, int NS>
 __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant__ SplitMaps maps, const SplitArgs a) {
     using L = ExpandLayout<R, NS>;
@@ -688,23 +684,19 @@ __global__ void __launch_bounds__(384, 1) expand_tc_kernel(const __grid_constant
         item_range(cm, bl, s_u, W.k0, W.k1);  // K1's output only: before the wait (see the shrink)
     }
     W.total = a.counters[PREFT_CTR_LORA_UNITS] * bl.nc;
-    tc::pdl_wait();  // P, y and the grab counter (reset by the previous launch) from here on
+    tc::pdl_wait();  // P, y and the launch-sequence counters from here on
+    LaunchSeq seq{0, nullptr};
+    if (a.sched) {
+        seq = launch_seq_begin(a.sched);
+        W.sched = seq.grab;
+    }
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1792 + 2 * blockIdx.x] = tc::globaltimer();
     SplitVSrc vs{static_cast<const float*>(a.P), a.ldp};
     expand_pipeline<R, NS>(maps, a, bl, sbase, sgen, tmem, B, W, vs);
     tc::fence_before_sync();
     __syncthreads();
     if (a.prof && tid == 0 && blockIdx.x < 128) a.prof[1793 + 2 * blockIdx.x] = tc::globaltimer();
-    if (tid == 0 && a.sched) {
-        // the last CTA out resets the grab counter (every CTA's producer took
-        // its last grab before its CTA got here)
-        __threadfence();
-        if (atomicAdd(a.sched + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-            a.sched[0] = 0;
-            a.sched[1] = 0;
-            __threadfence();
-        }
-    }
+    if (tid == 0 && a.sched) launch_seq_end(a.sched, seq.n);
     if (warp == 0) {
         __syncwarp();
         tc::tmem_dealloc(tmem, 512);

@@ -36,8 +36,8 @@ struct SplitArgs {
     long long plane_stride;
     int* sync;      // per-unit arrival counters (zero between launches)
     int flags;      // kSplitHints
-    int* sched;     // dynamic schedules (zero between launches): expand [0] next grab, [1] finished CTAs;
-                    //   LPT shrink [2], [3]; NULL = static ranges
+    int* sched;     // dynamic schedules: launch-sequence counters (LaunchSeq) of the expand at sched,
+                    //   of the LPT shrink at sched + kSeqInts; NULL = static ranges
     const int* unit_order;  // K1's size order of the LoRA units (PREFT_META_UNIT_ORDER)
     int grab;       // items per grab
     int beta_s;     // added to the shrink / expand cost models' per-column item overhead
@@ -66,7 +66,31 @@ constexpr int kPlanes = 4;                // max CTAs sharing one unit's shrink 
 constexpr int kBetaS = 128;
 constexpr int kBetaE = 128;
 constexpr int kSplitHints = 2;  // expand: Bt loads evict_last, y reduce-adds evict_first
-constexpr int kSchedInts = 8;   // the dynamic expand's counters in meta->lora_part
+constexpr int kMaxGrid = 1024;  // CTAs per launch the launch-sequence counters cover
+constexpr int kSeqInts = 8 + kMaxGrid;
+constexpr int kSchedInts = 2 * kSeqInts;  // the dynamic schedules' counters in meta->lora_part (expand, LPT shrink)
+
+// Launch-local counters without an end-of-kernel handshake.  Every CTA keeps
+// its own launch count at base[8 + blockIdx.x] — on one stream all CTAs of a
+// kernel's launches see the same count, so it numbers the launch — and grab
+// counters form a ring of three: launch n grabs from base[n % 3] and zeroes
+// base[(n + 2) % 3], which launch n - 1 used (it has completed: launches on a
+// stream run one after another past the PDL wait) and launch n + 2 will use.
+// The count is read after the PDL wait and written back by the CTA at its end;
+// the next launch reads it after its own wait.  The grid must not change
+// between launches that share a base.
+struct LaunchSeq {
+    int n;      // this launch's number
+    int* grab;  // this launch's grab counter
+};
+__device__ __forceinline__ LaunchSeq launch_seq_begin(int* base) {
+    const int n = *reinterpret_cast<volatile int*>(base + 8 + blockIdx.x);
+    if (blockIdx.x == 0 && threadIdx.x == 0) base[(n + 2) % 3] = 0;
+    return {n, base + n % 3};
+}
+__device__ __forceinline__ void launch_seq_end(int* base, int n) {  // one thread per CTA
+    base[8 + blockIdx.x] = n + 1;
+}
 
 struct SplitMaps {
     CUtensorMap x;       // x [rows][m] (this rank's columns), 16-row x 64-col boxes
