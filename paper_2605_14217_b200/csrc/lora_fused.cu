@@ -261,29 +261,26 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
     } else if (warp == 6) {
-        if (lane == 0) {
-            int stage = 0, pu = -1, slot = 0;
-            uint32_t phase = 0;
-            for (int k = s0; k < s1; ++k) {
-                const int u = k / ncs, g = k - u * ncs;
-                if (u != pu) {
-                    slot = a.units[u].x;
-                    pu = u;
-                }
-                const int np = bs.cw[0] / 64, p = g * np;
-                for (int pi = 0; pi < np; pi += kPps) {
-                    tc::mbar_wait(&empty[stage], phase ^ 1u);
-                    const uint32_t st = sbase + stage * LS::STAGE;
-#pragma unroll
-                    for (int pp = 0; pp < kPps; ++pp)
-#pragma unroll
-                        for (int s = 0; s < NS; ++s)
-                            tc::tma_load_2d(st + LS::X_BYTES + (pp * NS + s) * LS::AP_BYTES, &maps.A[s],
-                                            (p + pi + pp) * 64, slot * R, &full[stage]);
-                    if (++stage == LS::STAGES) {
-                        stage = 0;
-                        phase ^= 1u;
-                    }
+        int stage = 0, pu = -1, slot = 0;
+        uint32_t phase = 0;
+        const int pp = lane / NS, s = lane - pp * NS;  // lane-parallel box issue
+        for (int k = s0; k < s1; ++k) {
+            const int u = k / ncs, g = k - u * ncs;
+            if (u != pu) {
+                slot = a.units[u].x;
+                pu = u;
+            }
+            const int np = bs.cw[0] / 64, p = g * np;
+            for (int pi = 0; pi < np; pi += kPps) {
+                if (lane == 0) tc::mbar_wait(&empty[stage], phase ^ 1u);
+                __syncwarp();
+                const uint32_t st = sbase + stage * LS::STAGE;
+                if (lane < kPps * NS)
+                    tc::tma_load_2d(st + LS::X_BYTES + (pp * NS + s) * LS::AP_BYTES, &maps.A[s], (p + pi + pp) * 64,
+                                    slot * R, &full[stage]);
+                if (++stage == LS::STAGES) {
+                    stage = 0;
+                    phase ^= 1u;
                 }
             }
         }

@@ -250,10 +250,13 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
             }
         }
     } else if (warp == 6) {
-        // second producer: the adapters' A panels
-        if (lane == 0) {
+        // second producer: the adapters' A panels, lane (panel, site) issues one
+        // box, so a stage's kPps x NS boxes go out together (one thread issuing
+        // them back to back took ~100-200 cycles per box)
+        {
             int stage = 0, pu = -1, slot = 0;
             uint32_t phase = 0;
+            const int pp = lane / NS, s = lane - pp * NS;
             for (int k = k0; k < k1; ++k) {
                 const int u = k / nc, g = k - u * nc;
                 if (u != pu) {
@@ -262,14 +265,12 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_tc_kernel(const __gr
                 }
                 const int np = bl.cw[0] / 64, p = g * np;
                 for (int pi = 0; pi < np; pi += kPps) {
-                    tc::mbar_wait(&empty[stage], phase ^ 1u);
+                    if (lane == 0) tc::mbar_wait(&empty[stage], phase ^ 1u);
+                    __syncwarp();
                     const uint32_t st = sbase + stage * L::STAGE;
-#pragma unroll
-                    for (int pp = 0; pp < kPps; ++pp)
-#pragma unroll
-                        for (int s = 0; s < NS; ++s)
-                            tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s],
-                                            (p + pi + pp) * 64, slot * R, &full[stage]);
+                    if (lane < kPps * NS)
+                        tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s], (p + pi + pp) * 64,
+                                        slot * R, &full[stage]);
                     if (++stage == L::STAGES) {
                         stage = 0;
                         phase ^= 1u;
@@ -547,18 +548,16 @@ __global__ void __launch_bounds__(kShrinkThreads, 1) shrink_lpt_kernel(const __g
     } else if (warp == 6) {
         int stage = 0;
         uint32_t phase = 0;
+        const int pp = lane / NS, s = lane - pp * NS;  // lane-parallel box issue (see shrink_tc_kernel)
         walk([&](int u) {
-            if (lane != 0) return;
             const int slot = a.units[u].x;
             for (int p = 0; p < np; p += kPps) {
-                tc::mbar_wait(&empty[stage], phase ^ 1u);
+                if (lane == 0) tc::mbar_wait(&empty[stage], phase ^ 1u);
+                __syncwarp();
                 const uint32_t st = sbase + stage * L::STAGE;
-#pragma unroll
-                for (int pp = 0; pp < kPps; ++pp)
-#pragma unroll
-                    for (int s = 0; s < NS; ++s)
-                        tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s], (p + pp) * 64,
-                                        slot * R, &full[stage]);
+                if (lane < kPps * NS)
+                    tc::tma_load_2d(st + L::X_BYTES + (pp * NS + s) * L::AP_BYTES, &maps.A[s], (p + pp) * 64,
+                                    slot * R, &full[stage]);
                 if (++stage == L::STAGES) {
                     stage = 0;
                     phase ^= 1u;

@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--quick", action="store_true", help="whole steps only (no per-group / per-half lines)")
+    ap.add_argument("--empty", action="store_true", help="a batch of decode tokens only: the launches' fixed cost")
     ap.add_argument("--fused", default="", help="comma list of K-split pieces: also time the fused kernel")
     args = ap.parse_args()
     import torch
@@ -38,6 +39,8 @@ def main():
                        dtype=torch.bfloat16, device=dev, tp_rank=0, tp_size=args.tp)
     pool.fill_synthetic_(512, AdapterKind.LORA, r, seed=23, sigma=0.01)
     qsl, ids, flags, lens, _ = bench.step_entries(0, 1, 256, 256, seed=bench.SEED + 3)
+    if args.empty:
+        flags = flags | 1  # every entry a decode token of a prefill-only adapter: nothing selected
     slots = pool.entry_arrays(qsl, ids, flags)
     T = int(qsl[-1])
     meta = BatchMeta(len(ids), T, tile_tokens=128, device=dev)
