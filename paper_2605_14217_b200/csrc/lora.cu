@@ -256,7 +256,7 @@ int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, co
         // one rank: the exchange region is the tail of the meta's workspace
         preft_xchg_t xg;
         void* base = meta->lora_part + lora_split_floats(meta);
-        const int rc = xchg_init(&xg, &base, 1, 0, 4, meta->T_cap, meta->chunk_cap, 0);
+        const int rc = xchg_init(&xg, &base, 1, 0, 1, meta->T_cap, meta->chunk_cap, 0);
         if (rc) return rc;
         return lora_fused(meta, x, meta->T_cap, ldx, m, sites, nsites, r, dtype, &xg, stream, num_sms);
     }

@@ -177,7 +177,7 @@ class FusedExchange:
         return int(_lib.load().preft_xchg_region_bytes(tp, planes, meta.T_cap, meta.chunk_cap))
 
     @classmethod
-    def local(cls, meta, pool, planes: int = 4, grid: int = 0):
+    def local(cls, meta, pool, planes: int = 1, grid: int = 0):
         import torch
 
         n = (cls.region_bytes(meta, 1, planes) + 15) // 16 * 4
