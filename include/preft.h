@@ -230,8 +230,10 @@ int preft_lora_expand(const preft_meta_t* meta, const void* P, int64_t ldp, int6
                       const preft_lora_site_t* sites, int32_t nsites, int32_t r_max, int32_t dtype,
                       void* stream);
 /* Floats the tensor-core split wants in meta->lora_part (zero-initialised):
- * partial planes of P for units the shrink shares between CTAs, plus one
- * arrival counter per unit.  With less, every unit's shrink stays on one CTA. */
+ * P and its partial planes (K-split shrinks, opt-in), one arrival counter per
+ * unit, the dynamic schedules' launch-sequence counters (split.cuh LaunchSeq:
+ * without them every expand uses static ranges) and a one-rank exchange
+ * region for the opt-in fused route of preft_lora_apply (PREFT_LORA_FUSED=1). */
 int64_t preft_lora_part_floats(const preft_meta_t* meta);
 /*
  * Fused tensor-parallel LoRA^P: shrink -> cross-rank exchange of the rank-r
