@@ -222,16 +222,17 @@ int lora_fused(const preft_meta_t* meta, const void* x, long long rows, long lon
                const preft_lora_site_t* sites, int nsites, int r, int dtype, const preft_xchg_t* xg,
                cudaStream_t stream, int num_sms);
 
-// fused shrink -> expand (one launch, lora_fused.cu) for the r >= 16 route:
-// opt-in with PREFT_LORA_FUSED=1 — on one GPU the split pair with K-split
-// planes is faster (the fused kernel exists for the tensor-parallel exchange)
-static bool lora_fused_enabled() {
-    static int on = -1;
-    if (on < 0) {
+// fused shrink -> expand (one launch, lora_fused.cu) for the r >= 16 route
+// where it measured faster: inputs of >= 4096 columns (the 8B r16 step 14.58
+// -> 13.81 ms, bench lora16 line).  On narrow inputs (config-4 shards: m =
+// 1024) the split pair is faster.  PREFT_LORA_FUSED=0/1 forces off/on.
+static bool lora_fused_wanted(int m) {
+    static int on = -2;
+    if (on == -2) {
         const char* e = getenv("PREFT_LORA_FUSED");
-        on = (e && e[0] == '1') ? 1 : 0;
+        on = e ? (e[0] == '1' ? 1 : 0) : -1;
     }
-    return on == 1;
+    return on == 1 || (on == -1 && m >= 4096);
 }
 
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,
@@ -251,7 +252,7 @@ int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, co
     // rank-r intermediate in the meta's workspace (T x nsites x r f32, stays
     // in L2 between the two launches).  Both kernels only touch rows of the
     // K1 units, so the TMA bound T_cap never exposes rows beyond the batch.
-    if (lora_variant() != 0 && lora_fused_enabled() && meta->lora_part &&
+    if (lora_variant() != 0 && lora_fused_wanted(m) && meta->lora_part &&
         meta->lora_part_floats >= lora_part_floats_needed(meta) && lora_fused_ok(meta, x, ldx, m, sites, nsites, r, dtype)) {
         // one rank: the exchange region is the tail of the meta's workspace
         preft_xchg_t xg;

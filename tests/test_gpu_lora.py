@@ -312,3 +312,21 @@ def test_tensor_core_route_with_dynamic_grabs_forced():
                         str(root / "tests" / "test_gpu_lora.py"), "-k", "rank16_32_tensor_core_route"],
                        capture_output=True, text=True, timeout=600, cwd=root, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+def test_tensor_core_route_through_the_fused_kernel():
+    """preft_lora_apply's r >= 16 route through the fused kernel (one launch:
+    shrink -> one-rank exchange -> expand) on every eligible launch: the
+    route's parity and CUDA-graph checks rerun with PREFT_LORA_FUSED=1 (the
+    automatic choice takes it only for inputs of >= 4096 columns)."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    env = dict(os.environ, PREFT_LORA_FUSED="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
+                        str(root / "tests" / "test_gpu_lora.py"), "-k", "rank16_32_tensor_core_route"],
+                       capture_output=True, text=True, timeout=600, cwd=root, env=env)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
