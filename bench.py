@@ -1021,6 +1021,19 @@ def tp_config(args, device, world: int, rank: int, steps: int = 5) -> dict | Non
                                      exchange=fused_ex if fused_ex is not None else ex)
 
     s = torch.cuda.current_stream(device)
+    if ex is not None:
+        # the first real multi-GPU use of the exchange: a short wait bound, one
+        # layer probed first, and the NCCL path if any rank's wait timed out
+        ex.c.spin_ns = 200_000_000
+        for group in shapes.SITE_GROUPS:
+            x, ys = sets[0][group]
+            apply_lora_group_tp_(ys, x, meta, pool, 0, group, workspace=ws, stream=s, collective=real, exchange=ex)
+        bad = all_max(float(ex.errors()), world)
+        if bad:
+            exchange = "NCCL all-reduce (the fused exchange timed out on this group; fell back)"
+            barrier(world)
+            ex.close()
+            ex = None
     for _ in range(2):
         step(s)
     torch.cuda.synchronize()
