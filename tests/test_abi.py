@@ -97,3 +97,31 @@ def test_product_never_imports_the_oracle():
         text = f.read_text()
         assert "oracle" not in re.findall(r"^\s*(?:from|import)\s+(\w+)", text, flags=re.M), f
         assert "preft_oracle" not in text, f
+
+
+def test_exchange_region_layout_host_side():
+    """preft_xchg_init fills a rank's view of the fused kernel's exchange
+    regions exactly as include/preft.h lays them out (host-only: no device
+    memory is touched): partial planes, then the flags, then the state words."""
+    lib = _lib.load()
+    tp, planes, T_cap, U_cap = 4, 2, 96, 40
+    nbytes = lib.preft_xchg_region_bytes(tp, planes, T_cap, U_cap)
+    part = 2 * tp * planes * T_cap * 64 * 4
+    flags = 2 * tp * planes * U_cap * 4
+    assert nbytes >= part + flags + 64
+    bases = [0x10000000 * (r + 1) for r in range(tp)]
+    for rank in range(tp):
+        xg = _lib.PreftXchg()
+        arr = (ctypes.c_void_p * tp)(*bases)
+        assert lib.preft_xchg_init(ctypes.byref(xg), arr, tp, rank, planes, T_cap, U_cap, 1) == 0
+        assert (xg.tp_size, xg.tp_rank, xg.planes, xg.T_cap, xg.U_cap, xg.peer_sys) == (tp, rank, planes, T_cap, U_cap, 1)
+        assert [xg.part[d] for d in range(tp)] == bases
+        assert [xg.flag[d] for d in range(tp)] == [b + part for b in bases]
+        assert xg.state == bases[rank] + part + flags
+        assert xg.spin_ns > 0
+    # invalid layouts are rejected without touching anything
+    xg = _lib.PreftXchg()
+    assert lib.preft_xchg_init(ctypes.byref(xg), (ctypes.c_void_p * 2)(bases[0], bases[1] + 4), 2, 0, 1, T_cap,
+                               U_cap, 0) != 0  # misaligned peer base
+    assert lib.preft_xchg_init(ctypes.byref(xg), (ctypes.c_void_p * 9)(*([bases[0]] * 9)), 9, 0, 1, T_cap, U_cap,
+                               0) != 0  # more ranks than PREFT_XCHG_MAX_TP
