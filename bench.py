@@ -79,6 +79,8 @@ def parse(argv=None):
                    help="functional check of the multi-rank path on a 1-GPU box: every rank on cuda:0, gloo "
                         "for the bookkeeping collectives; the ranks time-share the GPU, so the numbers are not "
                         "scaling measurements")
+    p.add_argument("--eager", action="store_true",
+                   help="issue the timed steps from the host (default: the K steps replayed as one CUDA graph)")
     p.add_argument("--dry-run", action="store_true",
                    help="CPU/gloo launcher check: routing + collectives + the JSON line, no kernels")
     return p.parse_args(argv)
@@ -550,15 +552,26 @@ def time_steps(ctx, args, world, device, timing_tag=None):
     s = torch.cuda.current_stream(device)
     for _ in range(args.warmup):
         plan.run(s)
-    if timing_tag is not None:
-        plan.set_timing(timing_tag, args.steps * N_LAYERS + 8)
     torch.cuda.synchronize()
+    graph = None
+    if not args.eager:
+        # the K timed steps as ONE CUDA graph (K1 + every site launch of every
+        # step; the tagged launches' events as external event nodes), replayed
+        # once untimed and once timed
+        graph = plan.capture_steps(args.steps, timing_tag=timing_tag)
+        graph.replay()
+        torch.cuda.synchronize()
+    elif timing_tag is not None:
+        plan.set_timing(timing_tag, args.steps * N_LAYERS + 8)
     barrier(world)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(s)
-    for _ in range(args.steps):
-        plan.run(s)
+    if graph is not None:
+        graph.replay()
+    else:
+        for _ in range(args.steps):
+            plan.run(s)
     e1.record(s)
     torch.cuda.synchronize()
     barrier(world)
@@ -568,6 +581,7 @@ def time_steps(ctx, args, world, device, timing_tag=None):
         total, count = plan.collect_timing()
         plan.set_timing(-1, 0)
         kernel = (total, count)
+    del graph
     return ms, kernel
 
 

@@ -151,16 +151,22 @@ int preft_plan_run(preft_plan* p, int32_t run_meta, void* stream) {
         const int rc = meta_build(&p->meta, s, sms);
         if (rc) return rc < 0 ? plan_record_cuda(static_cast<cudaError_t>(-rc)) : rc;
     }
+    // under stream capture the timing events become external event-record
+    // nodes, re-recorded at every replay of the graph (so a graph of K steps
+    // yields its K steps' launch times)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (p->timing_tag >= 0) cudaStreamIsCapturing(s, &cap);
+    const unsigned rec_flags = cap == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : 0u;
     for (const PlanOp& op : p->ops) {
         const bool timed = p->timing_tag >= 0 && op.tag == p->timing_tag;
         if (timed) {
             if (p->used + 2 > p->pool.size()) return PREFT_ERR_STATE;  // reserve more pairs
-            cudaEventRecord(p->pool[p->used], s);
+            cudaEventRecordWithFlags(p->pool[p->used], s, rec_flags);
         }
         const int rc = plan_launch(p, op, s, sms);
         if (rc) return rc < 0 ? plan_record_cuda(static_cast<cudaError_t>(-rc)) : rc;
         if (timed) {
-            cudaEventRecord(p->pool[p->used + 1], s);
+            cudaEventRecordWithFlags(p->pool[p->used + 1], s, rec_flags);
             p->used += 2;
         }
     }

@@ -120,6 +120,25 @@ class StepPlan:
         if run_meta:
             self.meta.built_split = int(self.pool.slot_split)
 
+    def capture_steps(self, steps: int, stream=None, timing_tag: int | None = None) -> torch.cuda.CUDAGraph:
+        """Capture `steps` consecutive runs (K1 included) into ONE CUDA graph.
+        With a timing tag the tagged launches' events are captured as external
+        event-record nodes, so collect_timing() after a replay returns that
+        replay's per-launch times.  (`bench.py` times its K steps as one replay.)"""
+        s = stream if stream is not None else torch.cuda.Stream(self.pool.device)
+        s.wait_stream(torch.cuda.current_stream(self.pool.device))
+        with torch.cuda.stream(s):
+            self.run(s, True, _capturing=True)  # warm-up: occupancy queries, smem attributes
+        torch.cuda.current_stream(self.pool.device).wait_stream(s)
+        torch.cuda.synchronize(self.pool.device)
+        if timing_tag is not None:
+            self.set_timing(timing_tag, steps * max(1, self.n_ops) + 8)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(steps):
+                self.run(s, True, _capturing=True)
+        return g
+
     def capture(self, stream=None, run_meta: bool = True) -> torch.cuda.CUDAGraph:
         """Capture one run() into a CUDA graph (timing must be off).  With
         run_meta=False the graph holds only the site launches: the caller
