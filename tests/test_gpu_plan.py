@@ -113,3 +113,35 @@ def test_plan_graph_replay_is_bit_identical(cuda_device, run_meta):
         g.replay()
         torch.cuda.synchronize()
         _same(got, ref)
+
+
+def test_capture_steps_runs_k_steps_and_times_tagged_launches(cuda_device):
+    """StepPlan.capture_steps: K consecutive steps in one graph equal K eager
+    runs bit for bit, and the tagged launches' events (captured as external
+    event-record nodes) come back from collect_timing() after a replay."""
+    from paper_2605_14217_b200.plan import StepPlan
+
+    rng = np.random.default_rng(31)
+    pool, meta, qsl, slots, flags, acts = _setup(cuda_device, rng)
+    k = 3
+    eager = _clone(acts)
+    plan_e = _plan(pool, meta, eager)
+    for _ in range(k):
+        plan_e.run()
+    torch.cuda.synchronize()
+    got = _clone(acts)
+    plan = StepPlan(meta, pool)
+    for layer, (x, ys, yo, h) in enumerate(got):
+        plan.add_lora_group(ys, x, layer, ("Wq", "Wk", "Wv"), tag=1)
+        plan.add_lora_group([yo], x, layer, ("Wo",))
+        plan.add_reft(h, layer)
+    g = plan.capture_steps(k, timing_tag=1)  # its warm-up run edits the inputs: restore them
+    for (_, ys_g, yo_g, h_g), (_, ys0, yo0, h0) in zip(got, acts):
+        for dst, src in zip(ys_g + [yo_g, h_g], ys0 + [yo0, h0]):
+            dst.copy_(src)
+    torch.cuda.synchronize()
+    g.replay()
+    torch.cuda.synchronize()
+    _same(got, eager)
+    total, count = plan.collect_timing()
+    assert count == k * len(acts) and total > 0
