@@ -43,6 +43,17 @@ def main():
         ys = [U.rand_act(rng, T, sites[s][0], dtype, dev) for s in sites]
         h = U.rand_act(rng, T, d, dtype, dev)
         apply_lora_group_(ys, x, meta, pool, 0, tuple(sites))
+        if dtype == torch.bfloat16 and lr == 1:
+            # every K2 variant: the warp kernel and teams of 1 / 2 / 4 / 8 warps
+            lib = _lib.load()
+            for v in (0, 1, 2, 4, 8):
+                assert lib.preft_set_lora_variant(v) == 0
+                try:
+                    apply_lora_group_(ys, x, meta, pool, 0, tuple(sites))
+                    apply_lora_group_(ys[:1], x, meta, pool, 0, ("Wq",))
+                    torch.cuda.synchronize()
+                finally:
+                    lib.preft_set_lora_variant(-1)
         apply_lora_group_tp_(ys, x, meta, pool, 0, tuple(sites), workspace=SplitWorkspace(meta, pool))
         if dtype == torch.bfloat16 and lr == 16:
             # K2f, the fused shrink -> exchange -> expand kernel, one rank, whole and K-split units
