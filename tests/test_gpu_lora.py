@@ -296,6 +296,62 @@ def test_rank16_32_tensor_core_route(cuda_device, variant, rank):
         lib.preft_set_lora_variant(-1)
 
 
+def _edge_batch(kind):
+    """(qsl, ids, flags) of the edge batches the tcgen05 routes must handle."""
+    from paper_2605_14217_b200 import _lib
+
+    D = _lib.ENTRY_DECODE
+    if kind == "all_decode":  # nothing selected: every entry a decode token of a prefill-only adapter
+        lens, ids, fl = [1] * 24, [i % 10 for i in range(24)], [D] * 24
+    elif kind == "no_adapter":
+        lens, ids, fl = [7, 64, 1, 130], [None] * 4, [0, 0, D, 0]
+    elif kind == "one_long":  # one adapter, one long prompt: many units of the same adapter
+        lens, ids, fl = [1, 1, 1000, 1], [3, 4, 3, 3], [D, D, 0, D]
+    else:  # unit_edges: prompt lengths around the 16-row chunk and 64-row unit, repeated adapters
+        lens = [1, 15, 16, 17, 63, 64, 65, 128, 129, 1, 1]
+        ids = [0, 0, 1, 1, 2, 2, 3, 4, 4, 5, None]
+        fl = [0] * 9 + [D, 0]
+    qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    return qsl, ids, np.array(fl, np.int32)
+
+
+@pytest.mark.parametrize("kind", ["all_decode", "no_adapter", "one_long", "unit_edges"])
+def test_tensor_core_edge_batches(cuda_device, kind):
+    """The r = 16 tcgen05 route (split pair, or the fused kernel / dynamic grabs
+    in the subprocess reruns below) on edge batches: nothing selected, no
+    adapter at all, one long prompt of one adapter, and prompt lengths around
+    the chunk (16) and unit (64) boundaries.  Unselected rows bit-identical,
+    selected rows against the oracle."""
+    from paper_2605_14217_b200 import shapes
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_lora_group_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    rng = np.random.default_rng(7)
+    pool = AdapterPool(1, 512, lora_sites=TC_SITES, lora_capacity=10, lora_rank=16, dtype=torch.bfloat16,
+                       device=cuda_device)
+    for aid in range(10):
+        pool.register(U.random_lora_adapter(rng, aid, 1, TC_SITES, 16))
+    qsl, ids, flags = _edge_batch(kind)
+    meta = BatchMeta(len(ids), int(qsl[-1]), device=cuda_device)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    T = int(qsl[-1])
+    mask = U.oracle_mask(qsl, slots, flags)
+    for group in shapes.SITE_GROUPS:
+        x = U.rand_act(rng, T, TC_SITES[group[0]][1], torch.bfloat16, cuda_device)
+        ys = [U.rand_act(rng, T, TC_SITES[s][0], torch.bfloat16, cuda_device) for s in group]
+        y_in = [U.to_np(y) for y in ys]
+        apply_lora_group_(ys, x, meta, pool, 0, group)
+        torch.cuda.synchronize()
+        for s, y, yi in zip(group, ys, y_in):
+            out = U.to_np(y)
+            assert np.array_equal(out[~mask], yi[~mask]), (kind, s)
+            if mask.any():
+                ref = U.lora_oracle(yi, U.to_np(x), qsl, slots, flags, pool, 0, s)
+                helpers.check_close(out, yi, ref, "bf16", f"{kind} {s}")
+    meta.check_errors()
+
+
 def test_tensor_core_route_with_dynamic_grabs_forced():
     """The dynamic expand (item grabs from a global counter) on every TC
     launch, not only the wide groups it is chosen for: the r = 16/32 route's
@@ -309,7 +365,7 @@ def test_tensor_core_route_with_dynamic_grabs_forced():
     root = Path(__file__).resolve().parents[1]
     env = dict(os.environ, PREFT_SPLIT_DYN="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
-                        str(root / "tests" / "test_gpu_lora.py"), "-k", "rank16_32_tensor_core_route"],
+                        str(root / "tests" / "test_gpu_lora.py"), "-k", "rank16_32_tensor_core_route or tensor_core_edge"],
                        capture_output=True, text=True, timeout=600, cwd=root, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
 
@@ -327,6 +383,6 @@ def test_tensor_core_route_through_the_fused_kernel():
     root = Path(__file__).resolve().parents[1]
     env = dict(os.environ, PREFT_LORA_FUSED="1")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-p", "no:cacheprovider", "-m", "gpu",
-                        str(root / "tests" / "test_gpu_lora.py"), "-k", "rank16_32_tensor_core_route"],
+                        str(root / "tests" / "test_gpu_lora.py"), "-k", "rank16_32_tensor_core_route or tensor_core_edge"],
                        capture_output=True, text=True, timeout=600, cwd=root, env=env)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
