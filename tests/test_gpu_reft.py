@@ -250,3 +250,56 @@ def test_colaunch_eager_and_graph(cuda_device):
             assert torch.equal(h_g.view(torch.int16), h_co.view(torch.int16))
     finally:
         lib.preft_set_reft_variant(-1)
+
+
+@pytest.mark.parametrize("variant", [2, 3])
+@pytest.mark.parametrize("kind", ["all_decode", "no_adapter", "one_long", "unit_edges"])
+def test_tensor_core_edge_batches(cuda_device, variant, kind):
+    """The streaming (2) and resident (3) tcgen05 ReFT kernels at d = 2048,
+    r = 32 on edge batches: nothing selected, no adapter at all, one long
+    prompt of one adapter (many units of the same adapter back to back), and
+    prompt lengths around the chunk (16) and unit (64) boundaries.  Unselected
+    rows bit-identical, selected rows against the oracle."""
+    from paper_2605_14217_b200 import _lib
+    from paper_2605_14217_b200.meta import BatchMeta
+    from paper_2605_14217_b200.ops import apply_reft_
+    from paper_2605_14217_b200.pool import AdapterPool
+
+    d, rank = 2048, 32
+    D = _lib.ENTRY_DECODE
+    if kind == "all_decode":
+        lens, ids, fl = [1] * 24, [i % 6 for i in range(24)], [D] * 24
+    elif kind == "no_adapter":
+        lens, ids, fl = [7, 64, 1, 130], [None] * 4, [0, 0, D, 0]
+    elif kind == "one_long":
+        lens, ids, fl = [1, 1, 1000, 1], [3, 4, 3, 3], [D, D, 0, D]
+    else:
+        lens = [1, 15, 16, 17, 63, 64, 65, 128, 129, 1, 1]
+        ids = [0, 0, 1, 1, 2, 2, 3, 4, 4, 5, None]
+        fl = [0] * 9 + [D, 0]
+    qsl = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    flags = np.asarray(fl, dtype=np.int32)
+    rng = np.random.default_rng(11)
+    pool = AdapterPool(1, d, reft_capacity=6, reft_rank=rank, dtype=torch.bfloat16, device=cuda_device)
+    for aid in range(6):
+        kind_ = AdapterKind.DIREFT if aid % 2 else AdapterKind.LOREFT
+        pool.register(U.random_reft_adapter(rng, aid, 1, d, rank, kind_))
+    meta = BatchMeta(len(ids), int(qsl[-1]), device=cuda_device)
+    slots = U.stage(meta, pool, qsl, ids, flags)
+    T = int(qsl[-1])
+    h = U.rand_act(rng, T, d, torch.bfloat16, cuda_device)
+    h_in = U.to_np(h)
+    lib = _lib.load()
+    try:
+        assert lib.preft_set_reft_variant(variant) == 0
+        apply_reft_(h, meta, pool, 0)
+        torch.cuda.synchronize()
+    finally:
+        lib.preft_set_reft_variant(-1)
+    meta.check_errors()
+    mask = U.oracle_mask(qsl, slots, flags)
+    out = U.to_np(h)
+    assert np.array_equal(out[~mask], h_in[~mask])
+    if mask.any():
+        ref = U.reft_oracle(h_in, qsl, slots, flags, pool, 0)
+        helpers.check_close(out, h_in, ref, "bf16", f"reft {kind} variant {variant}")
