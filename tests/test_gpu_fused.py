@@ -131,7 +131,7 @@ def test_fused_graph_replay_bitwise(cuda_device):
     assert ex.errors() == 0
 
 
-def _tp_setup(cuda_device, tp, widths, seed):
+def _tp_setup(cuda_device, tp, widths, seed, batch=None):
     from paper_2605_14217_b200.meta import BatchMeta
 
     rng = np.random.default_rng(seed)
@@ -144,7 +144,7 @@ def _tp_setup(cuda_device, tp, widths, seed):
         full.register(ad)
         for p in shards:
             p.register(ad)
-    qsl, eids, flags = _batch(rng, ids)
+    qsl, eids, flags = _batch(rng, ids) if batch is None else batch(ids)
     T = int(qsl[-1])
     metas = [BatchMeta(64, T, device=cuda_device) for _ in range(tp)]
     slots = None
@@ -335,3 +335,60 @@ def test_fused_ipc_exchange_two_processes(cuda_device, tmp_path):
         ref = U.lora_oracle(yi, x.double().numpy(), qsl, slots, flags, full, 0, name)
         out = np.concatenate([outs[r][f"arr_{i}"] for r in range(2)], axis=1)
         helpers.check_close(out, yi, ref, "bf16", f"ipc tp=2 {name}")
+
+
+def _edge(kind):
+    def make(ids):
+        D = _lib.ENTRY_DECODE
+        if kind == "all_decode":
+            lens, e, fl = [1] * 24, [ids[i % len(ids)] for i in range(24)], [D] * 24
+        elif kind == "no_adapter":
+            lens, e, fl = [7, 64, 1, 130], [None] * 4, [0, 0, D, 0]
+        elif kind == "one_long":
+            lens, e, fl = [1, 1, 1000, 1], [ids[3], ids[4], ids[3], ids[3]], [D, D, 0, D]
+        else:
+            lens = [1, 15, 16, 17, 63, 64, 65, 128, 129, 1, 1]
+            e = [ids[i] for i in (0, 0, 1, 1, 2, 2, 3, 4, 4, 0)] + [None]
+            fl = [0] * 9 + [D, 0]
+        return np.concatenate([[0], np.cumsum(lens)]).astype(np.int32), e, np.asarray(fl, np.int32)
+    return make
+
+
+@pytest.mark.parametrize("planes", [1, 2])
+@pytest.mark.parametrize("kind", ["all_decode", "no_adapter", "one_long", "unit_edges"])
+def test_fused_tensor_parallel_edge_batches(cuda_device, kind, planes):
+    """Two emulated ranks through the fused kernel on edge batches: nothing
+    selected (every rank still publishes its flags and the launch tags stay in
+    step), no adapter at all, one long prompt of one adapter, and prompt
+    lengths around the chunk / unit boundaries."""
+    from paper_2605_14217_b200.tp import FusedExchange, apply_lora_group_tp_
+
+    tp = 2
+    rng, sites, full, shards, metas, qsl, slots, flags, T = _tp_setup(cuda_device, tp, (1024, 256, 2048), 77,
+                                                                     batch=_edge(kind))
+    mask = U.oracle_mask(qsl, slots, flags)
+    exs = FusedExchange.emulated(metas[0], shards[0], tp, planes=planes, grid=12)
+    streams = [torch.cuda.Stream() for _ in range(tp)]
+    for rep in range(2):  # both exchange parities
+        for group in GROUPS:
+            x_full = U.rand_act(rng, T, sites[group[0]][1], torch.bfloat16, cuda_device)
+            y_base = [U.rand_act(rng, T, sites[s][0], torch.bfloat16, cuda_device) for s in group]
+            xs, yss = _rank_acts(shards, group, x_full, y_base)
+            torch.cuda.synchronize()
+            for r in range(tp):
+                apply_lora_group_tp_(yss[r], xs[r], metas[r], shards[r], 0, group, exchange=exs[r],
+                                     stream=streams[r])
+            torch.cuda.synchronize()
+            sh = shards[0].lora_shard[group[0]]
+            for i, name in enumerate(group):
+                if sh.style == "column":
+                    out = np.concatenate([U.to_np(yss[r][i]) for r in range(tp)], axis=1)
+                else:
+                    out = sum(U.to_np(yss[r][i]) for r in range(tp))
+                yi = U.to_np(y_base[i])
+                assert np.array_equal(out[~mask], yi[~mask]), f"{kind} {name}: unselected rows touched"
+                if mask.any():
+                    ref = U.lora_oracle(yi, U.to_np(x_full), qsl, slots, flags, full, 0, name)
+                    helpers.check_close(out, yi, ref, "bf16", f"fused edge {kind} planes={planes} {name}")
+    for r in range(tp):
+        assert exs[r].errors() == 0, f"rank {r} timed out waiting for a peer"
