@@ -193,12 +193,13 @@ typedef struct preft_lora_site {
  *   {1,2,4,8,16,32,64} with nsites * r_max <= 64.
  * bf16 with r_max 16/32 (where the delta is a real contraction, ~10 FLOP/B
  * at r = 16), m % 256 == 0, every n % 128 == 0, every site's Bt_tc given and
- * meta->lora_part large enough runs on tcgen05: for inputs of >= 4096
+ * meta->lora_part large enough runs on tcgen05: for inputs of >= 8192
  * columns the fused kernel (preft_lora_fused with a one-rank exchange in
  * meta->lora_part: one launch), otherwise the split shrink into
  * meta->lora_part (L2-resident, T x nsites x r f32) then the split expand
  * (the kernels of preft_lora_shrink / preft_lora_expand, no collective).
- * PREFT_LORA_FUSED=0/1 forces either.
+ * PREFT_LORA_FUSED=0/1 forces either; PREFT_LORA_FUSED_MIN_M moves the
+ * threshold.
  * Everything else runs the SIMT kernels (team / warp per row).
  */
 int preft_lora_apply(const preft_meta_t* meta, const void* x, int64_t ldx, int32_t m,

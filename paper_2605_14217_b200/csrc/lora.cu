@@ -226,13 +226,20 @@ int lora_fused(const preft_meta_t* meta, const void* x, long long rows, long lon
 // where it measured faster: inputs of >= 4096 columns (the 8B r16 step 14.58
 // -> 13.81 ms, bench lora16 line).  On narrow inputs (config-4 shards: m =
 // 1024) the split pair is faster.  PREFT_LORA_FUSED=0/1 forces off/on.
+// The fused kernel (one launch: shrink -> one-rank exchange -> expand) for
+// inputs of >= 8192 columns, the split pair below that.  Measured at the 8B
+// r16 step (tools/split_breakdown.py --shape 8b --tp 1 --fused 1, r02h):
+// split / fused q/k/v (m 4096) 2.36 / 2.44 ms, o 1.61 / 1.60, gate/up 6.59 /
+// 6.61, down (m 14336) 3.22 / 3.07.  PREFT_LORA_FUSED=0/1 forces either
+// route, PREFT_LORA_FUSED_MIN_M moves the threshold.
 static bool lora_fused_wanted(int m) {
-    static int on = -2;
+    static int on = -2, min_m = 8192;
     if (on == -2) {
         const char* e = getenv("PREFT_LORA_FUSED");
         on = e ? (e[0] == '1' ? 1 : 0) : -1;
+        if (const char* t = getenv("PREFT_LORA_FUSED_MIN_M")) min_m = atoi(t);
     }
-    return on == 1 || (on == -1 && m >= 4096);
+    return on == 1 || (on == -1 && m >= min_m);
 }
 
 int lora_apply(const preft_meta_t* meta, const void* x, long long ldx, int m, const preft_lora_site_t* sites,

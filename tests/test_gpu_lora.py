@@ -374,7 +374,7 @@ def test_tensor_core_route_through_the_fused_kernel():
     """preft_lora_apply's r >= 16 route through the fused kernel (one launch:
     shrink -> one-rank exchange -> expand) on every eligible launch: the
     route's parity and CUDA-graph checks rerun with PREFT_LORA_FUSED=1 (the
-    automatic choice takes it only for inputs of >= 4096 columns)."""
+    automatic choice takes it only for inputs of >= 8192 columns)."""
     import os
     import subprocess
     import sys
